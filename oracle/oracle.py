@@ -74,6 +74,11 @@ def _bind(lib: C.CDLL) -> C.CDLL:
         "orc_enumerate_configs": (C.c_int, [C.c_int, _i64p, C.c_int, _i64p, C.c_int]),
         "orc_plan": (C.c_int, [vp, C.c_int, _i32p, C.POINTER(C.c_double), _i32p]),
         "orc_reduce": (C.c_int, [vp]),
+        "orc_rg_init": (C.c_int, [vp]),
+        "orc_rg_node": (C.c_int, [vp]),
+        "orc_rg_edge": (C.c_int, [vp]),
+        "orc_rg_edges_total": (C.c_int, [vp]),
+        "orc_rg_edge_info": (C.c_int, [vp, C.c_int, _i32p]),
         "orc_log_size": (C.c_int, [vp]),
         "orc_log_record": (C.c_int, [vp, C.c_int, _i32p]),
         "orc_log_argmin": (C.c_int, [vp, C.c_int, _i32p]),
@@ -261,6 +266,25 @@ class Instance:
     def reduce(self) -> "Instance":
         self._check(self.lib.orc_reduce(self.h))
         return self
+
+    # -- ReducedGraph step API ----------------------------------------------
+    def rg_init(self) -> "Instance":
+        self._check(self.lib.orc_rg_init(self.h))
+        return self
+
+    def node_elimination(self) -> bool:
+        return self.lib.orc_rg_node(self.h) == 1
+
+    def edge_elimination(self) -> bool:
+        return self.lib.orc_rg_edge(self.h) == 1
+
+    def live_edges(self):
+        out = []
+        info = np.zeros(3, np.int32)
+        for e in range(self.lib.orc_rg_edges_total(self.h)):
+            if self.lib.orc_rg_edge_info(self.h, e, info) == 0 and info[2]:
+                out.append((e, int(info[0]), int(info[1])))
+        return out
 
     def log(self):
         out = []

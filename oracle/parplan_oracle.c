@@ -1015,6 +1015,20 @@ static int edge_elimination(orc_instance *g) { /* :167-206 */
   return 1;
 }
 
+int orc_rg_init(orc_instance *g) { /* ReducedGraph ctor (:57-69) */
+  if (!g->have_tables) return set_err("no tables"), 1;
+  rg_init(g);
+  return 0;
+}
+int orc_rg_node(orc_instance *g) { return g->reduced ? node_elimination(g) : -1; }
+int orc_rg_edge(orc_instance *g) { return g->reduced ? edge_elimination(g) : -1; }
+int orc_rg_edges_total(const orc_instance *g) { return g->reduced ? g->n_redges : 0; }
+int orc_rg_edge_info(const orc_instance *g, int e, int32_t *info3) {
+  if (!g->reduced || e < 0 || e >= g->n_redges) return 1;
+  info3[0] = g->redges[e].src, info3[1] = g->redges[e].dst, info3[2] = g->redges[e].alive;
+  return 0;
+}
+
 int orc_reduce(orc_instance *g) { /* :209-217 */
   if (!g->have_tables) return set_err("no tables"), 1;
   rg_init(g);

@@ -87,6 +87,13 @@ int orc_enumerate_configs(int kind, const int64_t *shape, int device_count, int6
 int orc_plan(orc_instance *, int k_bound, int32_t *indices, double *cost, int32_t *stats);
 /* reduce only (:209-217), then log access */
 int orc_reduce(orc_instance *);
+/* ReducedGraph step API (:57-206): init, one node / edge elimination
+ * (returns 1 acted, 0 none), edge ids created so far, {src,dst,alive}. */
+int orc_rg_init(orc_instance *);
+int orc_rg_node(orc_instance *);
+int orc_rg_edge(orc_instance *);
+int orc_rg_edges_total(const orc_instance *);
+int orc_rg_edge_info(const orc_instance *, int edge, int32_t *info3);
 int orc_log_size(const orc_instance *);
 /* rec = {type(0 node,1 edge), removed, e1(in_edge), e2(out_edge), new_edge, src, dst} */
 int orc_log_record(const orc_instance *, int r, int32_t *rec7);

@@ -339,6 +339,51 @@ int orc_reduce(orc_instance *p) {
   });
 }
 
+int orc_rg_init(orc_instance *p) {
+  auto *i = reinterpret_cast<Inst *>(p);
+  return guard([&] { i->rg = std::make_unique<ReducedGraph>(i->graph, i->tables); });
+}
+int orc_rg_node(orc_instance *p) {
+  auto *i = reinterpret_cast<Inst *>(p);
+  return i->rg ? (i->rg->node_elimination() ? 1 : 0) : -1;
+}
+int orc_rg_edge(orc_instance *p) {
+  auto *i = reinterpret_cast<Inst *>(p);
+  return i->rg ? (i->rg->edge_elimination() ? 1 : 0) : -1;
+}
+int orc_rg_edges_total(const orc_instance *p) {
+  auto *i = reinterpret_cast<const Inst *>(p);
+  if (!i->rg) return 0;
+  int n = 0; // ids are dense: the largest id of any record + 1, or the original count
+  n = i->graph.edge_count();
+  for (const auto &rec : i->rg->log())
+    n = std::max(n, 1 + std::visit([](const auto &r) { return r.new_edge; }, rec));
+  return n;
+}
+int orc_rg_edge_info(const orc_instance *p, int e, int32_t *info3) {
+  auto *i = reinterpret_cast<const Inst *>(p);
+  if (!i->rg) return 1;
+  for (const auto &er : i->rg->live_edges())
+    if (er.id == e) {
+      info3[0] = er.src, info3[1] = er.dst, info3[2] = 1;
+      return 0;
+    }
+  // dead edge: recover endpoints from the graph or the log
+  if (e < i->graph.edge_count()) {
+    info3[0] = i->graph.edge(e).src, info3[1] = i->graph.edge(e).dst, info3[2] = 0;
+    return 0;
+  }
+  for (const auto &rec : i->rg->log()) {
+    int ne = std::visit([](const auto &r) { return r.new_edge; }, rec);
+    if (ne == e) {
+      std::visit([&](const auto &r) { info3[0] = r.src, info3[1] = r.dst; }, rec);
+      info3[2] = 0;
+      return 0;
+    }
+  }
+  return 1;
+}
+
 int orc_log_size(const orc_instance *p) {
   auto *i = reinterpret_cast<const Inst *>(p);
   return i->rg ? static_cast<int>(i->rg->log().size()) : 0;

@@ -1,0 +1,30 @@
+"""paper_1802_04924_b200 — B200-native search core of the layer-wise
+parallelization optimizer (arXiv 1802.04924, reference ``parplan``).
+
+The product is ``libparplan_cuda.so`` (C ABI: ``include/parplan_c.h``; C++
+drop-in headers: ``include/parplan/*.hpp``).  This package only binds it.
+"""
+from .capi import (  # noqa: F401
+    ComputationGraph,
+    Context,
+    CostTables,
+    CudaError,
+    DeviceGraph,
+    InputError,
+    Layer,
+    LimitError,
+    ParplanError,
+    PlanResult,
+    ReducedGraph,
+    brute_force_plan,
+    build_cost_tables,
+    builtin_model,
+    default_context,
+    device_count,
+    enumerate_final,
+    lib,
+    plan,
+    plan_with_tables,
+    synthetic_cost_tables,
+    upload_cost_tables,
+)

@@ -1,0 +1,115 @@
+// device.hpp — CUDA plumbing shared by the device translation units.
+#pragma once
+
+#include "internal.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#define PP_CUDA(call)                                                                                                  \
+  do {                                                                                                                 \
+    cudaError_t err_ = (call);                                                                                         \
+    if (err_ != cudaSuccess)                                                                                           \
+      ::pp::fail(PP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(err_));                                   \
+  } while (0)
+
+namespace pp {
+
+// Owning device allocation.
+template <class T> struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count) PP_CUDA(cudaMalloc(reinterpret_cast<void **>(&p), count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr, n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Pinned host staging buffer (grown on demand).
+struct PinnedBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf &) = delete;
+  PinnedBuf &operator=(const PinnedBuf &) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void *ensure(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      PP_CUDA(cudaMallocHost(&p, bytes));
+      cap = bytes;
+    }
+    return p;
+  }
+};
+
+// Packs heterogeneous host arrays into one byte image (16-byte aligned
+// sections) so a whole call's descriptors cross PCIe in one copy.
+struct Packer {
+  std::vector<unsigned char> bytes;
+  template <class T> size_t put(const T *src, size_t count) {
+    const size_t off = (bytes.size() + 15) & ~size_t(15);
+    bytes.resize(off + count * sizeof(T));
+    if (count) std::memcpy(bytes.data() + off, src, count * sizeof(T));
+    return off;
+  }
+  template <class T> size_t put(const std::vector<T> &v) { return put(v.data(), v.size()); }
+  size_t size() const { return bytes.size(); }
+};
+
+} // namespace pp
+
+// One CUDA device + stream; all calls on a context are stream-ordered and
+// synchronous at the API boundary.
+struct pp_context {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int precision = PP_PRECISION_AUTO;
+  int64_t launches = 0;
+  pp::DBuf<unsigned char> desc;  // device image of the current call's descriptors
+  pp::PinnedBuf staging;         // pinned host side of desc + results
+  pp::DBuf<unsigned char> scratch;
+
+  void begin() const; // cudaSetDevice + record ev0
+  double end_ms();    // record ev1, sync, elapsed
+  // uploads a packed descriptor image; returns its device base pointer
+  unsigned char *upload(const pp::Packer &pk);
+};
+
+namespace pp {
+inline void check_launch(pp_context *ctx, int n = 1) {
+  PP_CUDA(cudaGetLastError());
+  ctx->launches += n;
+}
+} // namespace pp

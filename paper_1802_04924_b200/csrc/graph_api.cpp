@@ -1,0 +1,168 @@
+// graph_api.cpp — host half of the C ABI: graphs, catalogs, the symbolic
+// schedule, error reporting.  No CUDA here; all of it works without a GPU.
+#include "internal.hpp"
+
+#include "parplan/models.hpp"
+
+#include <cstring>
+
+namespace pp {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string &m) { g_last_error = m; }
+
+Graph::Graph(parplan::ComputationGraph cg) : g(std::move(cg)) {
+  nl = g.layer_count();
+  ne = g.edge_count();
+  kind.resize(static_cast<size_t>(nl));
+  params.resize(static_cast<size_t>(nl) * 7);
+  shape.resize(static_cast<size_t>(nl) * 4);
+  rank.resize(static_cast<size_t>(nl));
+  for (int l = 0; l < nl; ++l) {
+    kind[static_cast<size_t>(l)] = static_cast<int32_t>(g.layer(l).kind.index());
+    parplan::detail::kind_params(g.layer(l).kind, &params[static_cast<size_t>(l) * 7]);
+    const auto s = parplan::detail::dims_of(g.shape(l));
+    std::memcpy(&shape[static_cast<size_t>(l) * 4], s.data(), 4 * sizeof(int64_t));
+    rank[static_cast<size_t>(l)] = g.topo_rank(l);
+  }
+  for (const parplan::Edge &e : g.edges()) {
+    esrc.push_back(e.src);
+    edst.push_back(e.dst);
+    epos.push_back(e.dst_input_pos);
+    band_offset.push_back(parplan::detail::concat_band_offset(g, e));
+  }
+}
+
+const Schedule &Graph::schedule() {
+  if (!sched) sched = std::make_unique<Schedule>(build_schedule(nl, esrc, edst, rank));
+  return *sched;
+}
+
+void enumerate_catalogs(const Graph &g, int devices, std::vector<int32_t> *counts, std::vector<int64_t> *configs) {
+  counts->clear();
+  configs->clear();
+  for (int l = 0; l < g.nl; ++l) {
+    const auto cat = parplan::enumerate_configs(g.g.layer(l).kind, g.g.shape(l), devices);
+    counts->push_back(static_cast<int32_t>(cat.size()));
+    for (const auto &c : cat) {
+      configs->push_back(c.sample);
+      configs->push_back(c.channel);
+      configs->push_back(c.height);
+      configs->push_back(c.width);
+    }
+  }
+}
+
+} // namespace pp
+
+using pp::guard;
+
+extern "C" {
+
+const char *pp_last_error(void) { return pp::g_last_error.c_str(); }
+int pp_abi_version(void) { return PP_ABI_VERSION; }
+
+pp_status pp_graph_create(const pp_graph_desc *d, pp_graph **out) {
+  return guard([&] {
+    PP_REQUIRE(d && out, "pp_graph_create: null argument");
+    PP_REQUIRE(d->n_layers >= 0 && d->n_edges >= 0, "pp_graph_create: negative sizes");
+    std::vector<parplan::Layer> layers;
+    std::vector<std::vector<std::string>> inputs(static_cast<size_t>(d->n_layers));
+    for (int l = 0; l < d->n_layers; ++l) {
+      std::string id = d->ids ? std::string(d->ids[l] ? d->ids[l] : "") : "n" + std::to_string(l);
+      layers.push_back({std::move(id), parplan::detail::kind_from_params(d->kind[l], d->params + 7 * l)});
+    }
+    int prev = 0;
+    for (int e = 0; e < d->n_edges; ++e) {
+      const int s = d->edge_src[e], t = d->edge_dst[e];
+      PP_REQUIRE(s >= 0 && s < d->n_layers && t >= 0 && t < d->n_layers,
+                 "edge " + std::to_string(e) + " references an undeclared layer");
+      PP_REQUIRE(t >= prev, "edges must be listed in destination order (the reference's dense edge ids)");
+      prev = t;
+      inputs[static_cast<size_t>(t)].push_back(layers[static_cast<size_t>(s)].id);
+    }
+    *out = new pp_graph(parplan::ComputationGraph::create(std::move(layers), inputs, d->batch));
+  });
+}
+
+pp_status pp_graph_builtin(const char *name, int64_t batch, pp_graph **out) {
+  return guard([&] {
+    PP_REQUIRE(name && out, "pp_graph_builtin: null argument");
+    *out = new pp_graph(parplan::builtin_model(name, batch));
+  });
+}
+
+pp_status pp_graph_destroy(pp_graph *g) {
+  delete g;
+  return PP_OK;
+}
+
+pp_status pp_graph_size(const pp_graph *g, int32_t *nl, int32_t *ne) {
+  return guard([&] {
+    PP_REQUIRE(g, "null graph");
+    if (nl) *nl = g->impl.nl;
+    if (ne) *ne = g->impl.ne;
+  });
+}
+
+pp_status pp_graph_layers(const pp_graph *g, int32_t *kind, int64_t *params, int64_t *shapes, int32_t *topo) {
+  return guard([&] {
+    PP_REQUIRE(g, "null graph");
+    const auto &G = g->impl;
+    if (kind) std::memcpy(kind, G.kind.data(), G.kind.size() * sizeof(int32_t));
+    if (params) std::memcpy(params, G.params.data(), G.params.size() * sizeof(int64_t));
+    if (shapes) std::memcpy(shapes, G.shape.data(), G.shape.size() * sizeof(int64_t));
+    if (topo)
+      for (int r = 0; r < G.nl; ++r) topo[r] = G.g.topo_order()[static_cast<size_t>(r)];
+  });
+}
+
+pp_status pp_graph_edges(const pp_graph *g, int32_t *src, int32_t *dst, int32_t *pos) {
+  return guard([&] {
+    PP_REQUIRE(g, "null graph");
+    const auto &G = g->impl;
+    for (int e = 0; e < G.ne; ++e) {
+      if (src) src[e] = G.esrc[static_cast<size_t>(e)];
+      if (dst) dst[e] = G.edst[static_cast<size_t>(e)];
+      if (pos) pos[e] = G.epos[static_cast<size_t>(e)];
+    }
+  });
+}
+
+pp_status pp_graph_layer_id(const pp_graph *g, int32_t l, char *buf, int32_t cap) {
+  return guard([&] {
+    PP_REQUIRE(g && buf && cap > 0, "pp_graph_layer_id: bad argument");
+    PP_REQUIRE(l >= 0 && l < g->impl.nl, "layer index out of range");
+    const std::string &id = g->impl.g.layer(l).id;
+    const size_t n = std::min(id.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, id.data(), n);
+    buf[n] = 0;
+  });
+}
+
+pp_status pp_graph_catalogs(const pp_graph *g, int32_t devices, int32_t *counts, int64_t *configs) {
+  return guard([&] {
+    PP_REQUIRE(g && counts, "pp_graph_catalogs: null argument");
+    std::vector<int32_t> c;
+    std::vector<int64_t> cfg;
+    pp::enumerate_catalogs(g->impl, devices, &c, &cfg);
+    std::memcpy(counts, c.data(), c.size() * sizeof(int32_t));
+    if (configs) std::memcpy(configs, cfg.data(), cfg.size() * sizeof(int64_t));
+  });
+}
+
+pp_status pp_graph_schedule(const pp_graph *g, int32_t *n, pp_record *recs, int32_t *n_waves) {
+  return guard([&] {
+    PP_REQUIRE(g && n, "pp_graph_schedule: null argument");
+    const pp::Schedule &s = const_cast<pp_graph *>(g)->impl.schedule();
+    *n = static_cast<int32_t>(s.ops.size());
+    if (n_waves) *n_waves = s.n_waves;
+    if (recs)
+      for (size_t k = 0; k < s.ops.size(); ++k) {
+        const pp::Op &o = s.ops[k];
+        recs[k] = pp_record{o.type, o.removed, o.e1, o.e2, o.ne, o.u, o.v, o.wave};
+      }
+  });
+}
+
+} // extern "C"

@@ -1,0 +1,83 @@
+// internal.hpp — shared internals of libparplan_cuda.so (not installed).
+#pragma once
+
+#include "parplan_c.h"
+#include "scheduler.hpp"
+
+#include "parplan/graph.hpp"
+#include "parplan/partition.hpp"
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace pp {
+
+// ---- errors -----------------------------------------------------------------
+
+struct Error : std::runtime_error {
+  pp_status code;
+  Error(pp_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(pp_status c, const std::string &m) { throw Error(c, m); }
+
+void set_last_error(const std::string &m);
+
+// Runs f, mapping exceptions to status codes + the thread-local message.
+template <class F> pp_status guard(F &&f) {
+  try {
+    f();
+    set_last_error("");
+    return PP_OK;
+  } catch (const Error &e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const parplan::LimitError &e) {
+    set_last_error(e.what());
+    return PP_ERR_LIMIT;
+  } catch (const parplan::InputError &e) {
+    set_last_error(e.what());
+    return PP_ERR_INPUT;
+  } catch (const std::bad_alloc &) {
+    set_last_error("out of host memory");
+    return PP_ERR_INTERNAL;
+  } catch (const std::exception &e) {
+    set_last_error(e.what());
+    return PP_ERR_INTERNAL;
+  }
+}
+
+#define PP_REQUIRE(cond, msg)                                                                                         \
+  do {                                                                                                                 \
+    if (!(cond)) ::pp::fail(PP_ERR_INPUT, msg);                                                                        \
+  } while (0)
+
+// ---- graph ------------------------------------------------------------------
+
+// A validated ComputationGraph plus the flat views the kernels consume.
+struct Graph {
+  parplan::ComputationGraph g;
+  int nl = 0, ne = 0;
+  std::vector<int32_t> kind;
+  std::vector<int64_t> params; // 7 per layer
+  std::vector<int64_t> shape;  // 4 per layer
+  std::vector<int> esrc, edst, epos, rank;
+  std::vector<int64_t> band_offset; // per edge, Concat destinations
+  std::unique_ptr<Schedule> sched;  // lazily built, topology-only
+
+  explicit Graph(parplan::ComputationGraph cg);
+  const Schedule &schedule();
+};
+
+// Catalogs of every layer (enumerate_configs) flattened: counts + 4 int64 each.
+void enumerate_catalogs(const Graph &g, int devices, std::vector<int32_t> *counts, std::vector<int64_t> *configs);
+
+} // namespace pp
+
+struct pp_graph {
+  pp::Graph impl;
+  explicit pp_graph(parplan::ComputationGraph cg) : impl(std::move(cg)) {}
+};

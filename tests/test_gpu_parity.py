@@ -1,0 +1,98 @@
+"""CUDA path vs the CPU oracle on the BASELINE configs (bit-exact).
+
+Tables: K1 xfer + K2 node costs against the restatement, compared as IEEE bit
+patterns.  Plans: indices, cost (bit-exact), elimination counts, the full
+log and every argmin table through the ReducedGraph step API.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from impls import bits
+
+pytestmark = pytest.mark.gpu
+
+BUILTINS = [("lenet5", 1), ("lenet5", 2), ("lenet5", 4), ("alexnet", 4), ("vgg16", 4), ("vgg16", 16),
+            ("inception_chain(3)", 2), ("inception_chain(3)", 8), ("inception_chain", 16)]
+
+
+@pytest.mark.parametrize("model,D", BUILTINS)
+def test_tables_bit_exact(gpu, model, D):
+    g = gpu.builtin(model, 32)
+    t = gpu.build_tables(g, D)
+    cat, node, xfer = gpu.tables(t)
+    comp, sync = gpu.analytic_split(t)
+    ref = O.Instance.builtin(model, 32, "port").build_tables(D)
+    for l in range(ref.n_layers):
+        assert (cat[l] == ref.catalog(l)).all()
+        assert (bits(node[l]) == bits(ref.node(l))).all(), f"node table of layer {l}"
+        assert (bits(comp[l]) == bits(ref.compute(l))).all()
+        assert (bits(sync[l]) == bits(ref.sync(l))).all()
+    for e in range(ref.n_edges):
+        assert (bits(xfer[e]) == bits(ref.xfer(e))).all(), f"xfer table of edge {e}"
+
+
+@pytest.mark.parametrize("model,D", BUILTINS)
+def test_plan_matches_oracle(gpu, model, D):
+    g = gpu.builtin(model, 32)
+    idx, cost, stats = gpu.plan(g, D)
+    want = O.Instance.builtin(model, 32, "port").build_tables(D).plan()
+    assert list(idx) == list(want.indices)
+    assert cost == want.cost
+    assert stats == (want.final_graph_nodes, want.node_eliminations, want.edge_eliminations)
+
+
+@pytest.mark.parametrize("model,D", [("alexnet", 4), ("vgg16", 16), ("inception_chain", 16)])
+def test_log_and_argmins(gpu, model, D):
+    g = gpu.builtin(model, 32)
+    t = gpu.build_tables(g, D)
+    rg = gpu.reduced(g, t)
+    rg.reduce()
+    ref = O.Instance.builtin(model, 32, "port").build_tables(D).reduce()
+    assert rg.log() == ref.log()
+    for r, rec in enumerate(ref.log()):
+        if rec[0] == 0:
+            assert (rg.argmin(r) == ref.log_argmin(r)).all(), f"argmin of record {r}"
+        assert (bits(rg.edge_table(rec[4])) == bits(ref.edge_table(rec[4]))).all(), f"table of edge {rec[4]}"
+
+
+def test_nonuniform_devices(gpu):
+    rng = np.random.default_rng(7)
+    D = 8
+    rates = rng.uniform(5e12, 2e13, D)
+    bw = rng.uniform(5e9, 5e10, D * D)
+    g = gpu.builtin("inception_chain(2)", 16)
+    t = gpu.build_tables(g, D, rates=rates, bw=bw)
+    _, node, xfer = gpu.tables(t)
+    ref = O.Instance.builtin("inception_chain(2)", 16, "port").build_tables(D, rates, bw)
+    assert all((bits(a) == bits(b)).all() for a, b in zip(node, ref.nodes()))
+    assert all((bits(a) == bits(b)).all() for a, b in zip(xfer, ref.xfers()))
+    idx, cost, _ = gpu.plan_with_tables(g, t)
+    want = ref.plan()
+    assert list(idx) == list(want.indices) and cost == want.cost
+
+
+@pytest.mark.parametrize("C", [4, 16, 64])
+def test_synthetic_config5_fixed_point(gpu, C):
+    """config-5 generator (N=1000, bp=0.3, seed 1): exact int32 fixed-point DP."""
+    g, t = gpu.synthetic(1, 1000, C)
+    idx, cost, stats = gpu.plan_with_tables(g, t)
+    ref = O.Instance.synthetic(1, 1000, C, 0.3, "port")
+    want = ref.plan()
+    assert list(idx) == list(want.indices)
+    assert cost == want.cost
+    assert stats == (want.final_graph_nodes, want.node_eliminations, want.edge_eliminations)
+
+
+def test_fp64_and_fixed_point_agree(gpu):
+    import paper_1802_04924_b200 as P
+
+    inst = O.Instance.synthetic(3, 300, 24, 0.3, "port")
+    g = gpu._graph_of(inst)
+    ctx64 = P.Context(0, precision="fp64")
+    t_fix = P.upload_cost_tables(g, inst.catalogs(), inst.nodes(), inst.xfers(), gpu.ctx)
+    t_64 = P.upload_cost_tables(g, inst.catalogs(), inst.nodes(), inst.xfers(), ctx64)
+    a = P.plan_with_tables(g, t_fix)
+    b = P.plan_with_tables(g, t_64)
+    assert a.precision == "fixed" and b.precision == "fp64"
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost == inst.plan().cost
