@@ -81,6 +81,7 @@ typedef struct pp_context pp_context;
 typedef struct pp_graph pp_graph;
 typedef struct pp_tables pp_tables;
 typedef struct pp_reduced pp_reduced;
+typedef struct pp_prepared pp_prepared;
 
 /* A computation graph as flat arrays (ComputationGraph::create inputs).
  * Edges are listed in creation order: by destination layer ascending, then by
@@ -113,6 +114,8 @@ typedef struct pp_plan_result {
   int32_t waves;     /* dependency waves the schedule executed in */
   int32_t launches;  /* kernel launches issued by this call */
   double device_ms;  /* CUDA-event time of the device work of this call */
+  int64_t h2d_bytes; /* host->device bytes the call copied (descriptor image) */
+  int64_t d2h_bytes; /* device->host bytes (indices + cost) */
 } pp_plan_result;
 
 /* One elimination record (planner.hpp:32-45). type 0 = node, 1 = edge. */
@@ -135,6 +138,10 @@ pp_status pp_device_count(int32_t *count);
 
 /* ---- context ---------------------------------------------------------- */
 pp_status pp_context_create(int32_t device, pp_context **out);
+/* Same, but every call is ordered on the caller's cudaStream_t (e.g. a
+ * PyTorch stream), so the caller's CUDA events time the planner's work. */
+pp_status pp_context_create_on_stream(int32_t device, void *cuda_stream, pp_context **out);
+pp_status pp_context_stream(const pp_context *ctx, void **cuda_stream);
 pp_status pp_context_destroy(pp_context *ctx);
 pp_status pp_context_set_precision(pp_context *ctx, int32_t policy);
 /* kernel launches issued on this context since creation */
@@ -158,6 +165,17 @@ pp_status pp_graph_catalogs(const pp_graph *g, int32_t device_count, int32_t *co
  * O((N+E) log N) host scheduler: the exact record sequence reduce() logs.
  * records may be NULL (size query). */
 pp_status pp_graph_schedule(const pp_graph *g, int32_t *n_records, pp_record *records, int32_t *n_waves);
+
+/* ---- seeded instances (oracle.hpp:98-185) ------------------------------- */
+/* Series-parallel topology of random_series_parallel_graph for `seed`
+ * (std::mt19937_64, the reference's draw order), without tables. */
+pp_status pp_graph_series_parallel(uint64_t seed, int32_t node_count, double branch_probability, pp_graph **out);
+/* random_series_parallel_graph (graph + dyadic tables, uploaded).  With
+ * configs_override > 0 every catalog is C dummy configs {1,1,1,i+1} instead
+ * of the truncated enumeration (the config-5 sweep generator). */
+pp_status pp_random_instance(pp_context *ctx, uint64_t seed, int32_t node_count, int32_t max_configs,
+                             double branch_probability, int32_t device_count, int32_t configs_override,
+                             pp_graph **graph, pp_tables **tables);
 
 /* ---- cost tables (device) ----------------------------------------------- */
 /* build_cost_tables (cost.hpp:170-206): K2 node-cost fill + K1 xfer builder. */
@@ -188,6 +206,26 @@ pp_status pp_plan(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev,
 /* plan_with_tables() (planner.hpp:339-366) */
 pp_status pp_plan_with_tables(pp_context *ctx, const pp_graph *g, pp_tables *t, int32_t k_bound, int32_t *indices,
                               pp_plan_result *res);
+/* Prepared plans — for callers that re-plan the same graph: the host work
+ * (catalogs, the symbolic schedule, the memory plan, every launch descriptor)
+ * runs once in prepare; launch enqueues only device work (one CUDA graph:
+ * K1/K2 when built from a device graph, one wave kernel per dependency wave,
+ * K5, unwind + cost re-sum, and the D2H of the result), optionally preceded by
+ * the H2D of the descriptor image (upload_inputs != 0); fetch waits and
+ * returns what pp_plan returns.  Give exactly one of dev / t. */
+pp_status pp_plan_prepare(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev, pp_tables *t, int32_t k_bound,
+                          pp_prepared **out);
+pp_status pp_plan_launch(pp_prepared *p, int32_t upload_inputs);
+pp_status pp_plan_fetch(pp_prepared *p, int32_t *indices, pp_plan_result *res);
+pp_status pp_plan_destroy(pp_prepared *p);
+/* Runs the prepared device work once with a CUDA event between launches and
+ * reports, per step: device ms, kind (0 K1/K2 tables, 1 wave of K3/K4 folds
+ * and merges, 2 K5 enumeration, 3 unwind + cost re-sum, 4 result D2H) and
+ * algorithmic work (table cells for 0; sum of nu*nw*nv fold cells plus merge
+ * cells for 1; candidates for 2; bytes for 4).  n_steps receives the count. */
+pp_status pp_plan_profile(pp_prepared *p, int32_t cap, double *step_ms, int32_t *step_kind, double *step_work,
+                          int32_t *n_steps);
+
 /* evaluate_strategy by index (cost.hpp:235-255), computed on the device from the
  * device-resident tables in the pinned summation order. */
 pp_status pp_tables_total_cost(pp_tables *t, const int32_t *indices, double *cost);

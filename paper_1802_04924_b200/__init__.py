@@ -15,6 +15,7 @@ from .capi import (  # noqa: F401
     LimitError,
     ParplanError,
     PlanResult,
+    PreparedPlan,
     ReducedGraph,
     brute_force_plan,
     build_cost_tables,

@@ -52,7 +52,8 @@ class _Record(C.Structure):
 class _PlanResult(C.Structure):
     _fields_ = [("cost", C.c_double), ("final_graph_nodes", C.c_int32), ("node_eliminations", C.c_int32),
                 ("edge_eliminations", C.c_int32), ("precision", C.c_int32), ("waves", C.c_int32),
-                ("launches", C.c_int32), ("device_ms", C.c_double)]
+                ("launches", C.c_int32), ("device_ms", C.c_double), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64)]
 
 
 class _GraphDesc(C.Structure):
@@ -75,6 +76,13 @@ _SIGS = {
     "pp_abi_version": (C.c_int, []),
     "pp_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "pp_context_create": (C.c_int, [C.c_int32, _pp]),
+    "pp_context_create_on_stream": (C.c_int, [C.c_int32, _vp, _pp]),
+    "pp_context_stream": (C.c_int, [_vp, _pp]),
+    "pp_plan_prepare": (C.c_int, [_vp, _vp, C.c_void_p, _vp, C.c_int32, _pp]),
+    "pp_plan_launch": (C.c_int, [_vp, C.c_int32]),
+    "pp_plan_fetch": (C.c_int, [_vp, _i32p, C.POINTER(_PlanResult)]),
+    "pp_plan_destroy": (C.c_int, [_vp]),
+    "pp_plan_profile": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, C.POINTER(C.c_int32)]),
     "pp_context_destroy": (C.c_int, [_vp]),
     "pp_context_set_precision": (C.c_int, [_vp, C.c_int32]),
     "pp_context_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
@@ -87,6 +95,9 @@ _SIGS = {
     "pp_graph_layer_id": (C.c_int, [_vp, C.c_int32, C.c_char_p, C.c_int32]),
     "pp_graph_catalogs": (C.c_int, [_vp, C.c_int32, _i32p, _vp]),
     "pp_graph_schedule": (C.c_int, [_vp, C.POINTER(C.c_int32), _vp, C.POINTER(C.c_int32)]),
+    "pp_graph_series_parallel": (C.c_int, [C.c_uint64, C.c_int32, C.c_double, _pp]),
+    "pp_random_instance": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, _pp,
+                                     _pp]),
     "pp_tables_build": (C.c_int, [_vp, _vp, C.POINTER(_DeviceDesc), _pp]),
     "pp_tables_upload": (C.c_int, [_vp, _vp, _i32p, _vp, _f64p, _f64p, _pp]),
     "pp_tables_synthetic": (C.c_int, [_vp, _vp, C.c_int32, C.c_uint64, _pp]),
@@ -165,9 +176,14 @@ def device_count() -> int:
 class Context:
     """One CUDA device + stream (pp_context)."""
 
-    def __init__(self, device: int = 0, precision: str = "auto"):
+    def __init__(self, device: int = 0, precision: str = "auto", stream: Optional[int] = None):
+        """stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
+        to order every planner call on, so the caller's CUDA events time it."""
         h = C.c_void_p()
-        _check(lib().pp_context_create(device, C.byref(h)))
+        if stream is None:
+            _check(lib().pp_context_create(device, C.byref(h)))
+        else:
+            _check(lib().pp_context_create_on_stream(device, C.c_void_p(stream), C.byref(h)))
         self.h = h
         self.device = device
         if precision != "auto":
@@ -440,6 +456,32 @@ def synthetic_cost_tables(graph: ComputationGraph, configs: int, seed: int, ctx:
     return CostTables(ctx, graph, h)
 
 
+def series_parallel_graph(seed: int, node_count: int, bp: float = 0.3) -> ComputationGraph:
+    """Topology of random_series_parallel_graph (oracle.hpp:130-157)."""
+    h = C.c_void_p()
+    _check(lib().pp_graph_series_parallel(seed, node_count, bp, C.byref(h)))
+    return ComputationGraph(h)
+
+
+def random_series_parallel_graph(seed: int, node_count: int = 6, max_configs: int = 3, bp: float = 0.3,
+                                 device_count: int = 4, ctx: Optional[Context] = None):
+    """oracle.hpp:121-185 -> (graph, device tables)."""
+    ctx = ctx or default_context()
+    g, t = C.c_void_p(), C.c_void_p()
+    _check(lib().pp_random_instance(ctx.h, seed, node_count, max_configs, bp, device_count, 0, C.byref(g), C.byref(t)))
+    graph = ComputationGraph(g)
+    return graph, CostTables(ctx, graph, t)
+
+
+def synthetic_instance(seed: int, node_count: int, configs: int, bp: float = 0.3, ctx: Optional[Context] = None):
+    """Config-5 generator (reference draw order, C dummy configs per layer) -> (graph, device tables)."""
+    ctx = ctx or default_context()
+    g, t = C.c_void_p(), C.c_void_p()
+    _check(lib().pp_random_instance(ctx.h, seed, node_count, 1, bp, 1, configs, C.byref(g), C.byref(t)))
+    graph = ComputationGraph(g)
+    return graph, CostTables(ctx, graph, t)
+
+
 @dataclass
 class PlanResult:
     """PlanResult (planner.hpp:325-334) + device accounting."""
@@ -459,8 +501,10 @@ class PlanResult:
 
 
 def _result(idx, r: _PlanResult) -> PlanResult:
-    return PlanResult(idx, r.cost, r.final_graph_nodes, r.node_eliminations, r.edge_eliminations,
-                      "fp64" if r.precision == 1 else "fixed", r.waves, r.launches, r.device_ms)
+    out = PlanResult(idx, r.cost, r.final_graph_nodes, r.node_eliminations, r.edge_eliminations,
+                     "fp64" if r.precision == 1 else "fixed", r.waves, r.launches, r.device_ms)
+    out.h2d_bytes, out.d2h_bytes = r.h2d_bytes, r.d2h_bytes
+    return out
 
 
 def plan_with_tables(graph: ComputationGraph, tables: CostTables, k_bound: int = 8) -> PlanResult:
@@ -477,6 +521,46 @@ def plan(graph: ComputationGraph, devices: DeviceGraph, k_bound: int = 8, ctx: O
     d = devices._desc()
     _check(lib().pp_plan(ctx.h, graph.h, C.byref(d), k_bound, idx, C.byref(r)))
     return _result(idx, r)
+
+
+class PreparedPlan:
+    """pp_plan_prepare: host work once, then launch() = device work only."""
+
+    def __init__(self, graph: ComputationGraph, devices: Optional[DeviceGraph] = None,
+                 tables: Optional[CostTables] = None, k_bound: int = 8, ctx: Optional[Context] = None):
+        self.ctx = tables.ctx if tables is not None else (ctx or default_context())
+        self.graph, self.tables = graph, tables
+        h = C.c_void_p()
+        d = devices._desc() if devices is not None else None
+        self._dev = devices
+        _check(lib().pp_plan_prepare(self.ctx.h, graph.h, C.cast(C.pointer(d), C.c_void_p) if d is not None else None,
+                                     tables.h if tables is not None else None, k_bound, C.byref(h)))
+        self.h = h
+
+    def launch(self, upload_inputs: bool = False) -> None:
+        _check(lib().pp_plan_launch(self.h, 1 if upload_inputs else 0))
+
+    def fetch(self) -> PlanResult:
+        idx = np.zeros(self.graph.n_layers, np.int32)
+        r = _PlanResult()
+        _check(lib().pp_plan_fetch(self.h, idx, C.byref(r)))
+        out = _result(idx, r)
+        out.h2d_bytes, out.d2h_bytes = r.h2d_bytes, r.d2h_bytes
+        return out
+
+    def profile(self):
+        """[(kind, device_ms, work)] for one run with events between launches."""
+        n = C.c_int32()
+        _check(lib().pp_plan_profile(self.h, 0, None, None, None, C.byref(n)))
+        ms, kind, work = np.zeros(n.value), np.zeros(n.value, np.int32), np.zeros(n.value)
+        _check(lib().pp_plan_profile(self.h, n.value, _ptr(ms), _ptr(kind), _ptr(work), C.byref(n)))
+        names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h"}
+        return [(names[int(k)], float(m), float(w)) for k, m, w in zip(kind, ms, work)]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().pp_plan_destroy(self.h)
+            self.h = None
 
 
 def brute_force_plan(graph: ComputationGraph, tables: CostTables, budget: int = 10_000_000):

@@ -18,19 +18,20 @@
 
 namespace pp {
 
-// Owning device allocation.
+// Device allocation: owning (alloc/ensure) or a non-owning view into a pool.
 template <class T> struct DBuf {
   T *p = nullptr;
   size_t n = 0;
+  bool own = true;
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   DBuf(const DBuf &) = delete;
   DBuf &operator=(const DBuf &) = delete;
-  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), own(o.own) { o.p = nullptr, o.n = 0; }
   DBuf &operator=(DBuf &&o) noexcept {
     if (this != &o) {
       release();
-      p = o.p, n = o.n;
+      p = o.p, n = o.n, own = o.own;
       o.p = nullptr, o.n = 0;
     }
     return *this;
@@ -38,15 +39,20 @@ template <class T> struct DBuf {
   ~DBuf() { release(); }
   void alloc(size_t count) {
     release();
+    own = true;
     if (count) PP_CUDA(cudaMalloc(reinterpret_cast<void **>(&p), count * sizeof(T)));
     n = count;
   }
   void ensure(size_t count) {
-    if (count > n) alloc(count);
+    if (count > n || !own) alloc(count);
+  }
+  void view(void *ptr, size_t count) {
+    release();
+    p = static_cast<T *>(ptr), n = count, own = false;
   }
   void release() {
-    if (p) cudaFree(p);
-    p = nullptr, n = 0;
+    if (p && own) cudaFree(p);
+    p = nullptr, n = 0, own = true;
   }
   size_t bytes() const { return n * sizeof(T); }
 };
@@ -94,12 +100,17 @@ struct pp_context {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
+  bool external_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int precision = PP_PRECISION_AUTO;
   int64_t launches = 0;
   pp::DBuf<unsigned char> desc;  // device image of the current call's descriptors
   pp::PinnedBuf staging;         // pinned host side of desc + results
   pp::DBuf<unsigned char> scratch;
+  // grow-only pools for one-shot plans (pp_plan / pp_plan_with_tables): no
+  // cudaMalloc/cudaFree on the steady-state path
+  pp::DBuf<unsigned char> plan_pool;
+  pp::PinnedBuf plan_pinned;
 
   void begin() const; // cudaSetDevice + record ev0
   double end_ms();    // record ev1, sync, elapsed

@@ -7,8 +7,10 @@
 
 namespace pp {
 
-// plan_with_tables on the device: waves of K3/K4, K5, unwind, cost re-sum.
-void run_plan(pp_context *ctx, Graph &g, Tables &t, int k_bound, int32_t *indices, pp_plan_result *res);
+// plan_with_tables (t given) or plan (dev given: K1/K2 first) on the device:
+// waves of K3/K4, K5, unwind, cost re-sum — one-shot, from the context pools.
+void run_plan(pp_context *ctx, Graph &g, Tables *t, const pp_device_desc *dev, int k_bound, int32_t *indices,
+              pp_plan_result *res);
 
 // K5 over an explicit node/edge list (ReducedGraph::enumerate_final, brute force).
 void run_enumerate(pp_context *ctx, int mode, int shift, const std::vector<const void *> &node_tabs,

@@ -1,0 +1,569 @@
+// plan.cu — the batched plan executor: plan() / plan_with_tables() on the device.
+//
+// prepare (host, once):  catalogs + K1/K2 descriptors (plan()), the cached
+//                        symbolic schedule, a liveness memory plan for derived
+//                        tables, and ONE descriptor image holding every launch's
+//                        work list plus the result slots
+// launch  (device only): [H2D image] -> K1/K2 -> one wave kernel per dependency
+//                        wave -> K5 enumerate -> finish (unwind + cost re-sum)
+//                        -> D2H of indices + cost; captured as a CUDA graph
+//                        for prepared plans
+// fetch:                 stream sync, parse results
+#include "dp.hpp"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <map>
+
+namespace pp {
+
+namespace {
+
+// First-fit offset allocator with coalescing; derived tables are released
+// after the wave that consumes them (never reused inside that wave).
+class OffsetPlanner {
+public:
+  size_t alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+      if (it->second >= bytes) {
+        const size_t off = it->first, rest = it->second - bytes;
+        free_.erase(it);
+        if (rest) free_[off + bytes] = rest;
+        return off;
+      }
+    const size_t off = end_;
+    end_ += bytes;
+    return off;
+  }
+  void release(size_t off, size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    auto it = free_.emplace(off, bytes).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) it->second += nx->second, free_.erase(nx);
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) pv->second += it->second, free_.erase(it);
+    }
+  }
+  size_t end() const { return end_; }
+
+private:
+  std::map<size_t, size_t> free_;
+  size_t end_ = 0;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+} // namespace
+} // namespace pp
+
+using namespace pp;
+
+struct pp_prepared {
+  pp_context *ctx = nullptr;
+  Graph *g = nullptr;
+  Tables *t = nullptr;
+  std::unique_ptr<Tables> own_t;
+  bool transient = true;
+  DBuf<unsigned char> dmem;
+  PinnedBuf hmem;
+  unsigned char *dbase = nullptr, *hbase = nullptr;
+  size_t image_off = 0, image_bytes = 0, res_off = 0, res_bytes = 0, off_idx = 0, off_cost = 0;
+  std::vector<std::function<void(cudaStream_t)>> steps;
+  int launches_per_run = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int K = 0, n_waves = 0, node_ops = 0, edge_ops = 0;
+  std::vector<int32_t> step_kind; // 0 K1/K2, 1 wave, 2 K5, 3 finish, 4 D2H
+  std::vector<double> step_work;  // cells: K1/K2 table cells, wave min-plus cells (nu*nw*nv) + merge cells
+  bool launched = false, uploaded = false;
+
+  ~pp_prepared() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+
+namespace pp {
+
+template <class T>
+static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
+  pp_context *ctx = P->ctx;
+  Graph &g = *P->g;
+  Tables &t = *P->t;
+  const Schedule &s = g.schedule();
+  const int K = static_cast<int>(s.final_nodes.size());
+  if (K > k_bound)
+    throw parplan::LimitError("final graph has " + std::to_string(K) + " nodes, exceeding the enumeration bound of " +
+                              std::to_string(k_bound) + " (graph is not reducible enough)");
+  PP_REQUIRE(K <= kMaxEnumNodes, "final graph too large for the enumeration kernel");
+  P->K = K;
+  P->n_waves = s.n_waves;
+  P->node_ops = s.node_ops;
+  P->edge_ops = s.edge_ops;
+
+  const int E_total = static_cast<int>(s.esrc.size());
+  std::vector<int32_t> rows(static_cast<size_t>(E_total)), cols(static_cast<size_t>(E_total));
+  for (int id = 0; id < E_total; ++id) {
+    rows[static_cast<size_t>(id)] = t.counts[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])];
+    cols[static_cast<size_t>(id)] = t.counts[static_cast<size_t>(s.edst[static_cast<size_t>(id)])];
+  }
+  for (const Op &op : s.ops)
+    if (!op.type) PP_REQUIRE(t.counts[static_cast<size_t>(op.removed)] <= 65535, "argmin index exceeds 16 bits");
+
+  // ---- memory plan ----------------------------------------------------------
+  auto cells = [&](int id) { return static_cast<size_t>(rows[static_cast<size_t>(id)]) * cols[static_cast<size_t>(id)]; };
+  size_t derived_total = 0;
+  for (const Op &op : s.ops) derived_total += align256(cells(op.ne) * sizeof(T));
+  const bool keep_all = derived_total <= (size_t(4) << 30);
+  OffsetPlanner tab_plan;
+  std::vector<size_t> tab_off(static_cast<size_t>(E_total), 0), am_off(s.ops.size(), 0);
+  size_t am_bytes = 0;
+  for (int w = 1; w <= s.n_waves; ++w) {
+    const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
+    for (int x = x0; x < x1; ++x) {
+      const int oi = s.exec[static_cast<size_t>(x)];
+      const Op &op = s.ops[static_cast<size_t>(oi)];
+      tab_off[static_cast<size_t>(op.ne)] = tab_plan.alloc(cells(op.ne) * sizeof(T));
+      if (!op.type) {
+        am_off[static_cast<size_t>(oi)] = am_bytes;
+        am_bytes += align256(cells(op.ne) * 2);
+      }
+    }
+    if (!keep_all)
+      for (int x = x0; x < x1; ++x) {
+        const Op &op = s.ops[static_cast<size_t>(s.exec[static_cast<size_t>(x)])];
+        for (int in : {op.e1, op.e2})
+          if (in >= t.ne) tab_plan.release(tab_off[static_cast<size_t>(in)], cells(in) * sizeof(T));
+      }
+  }
+  const size_t tables_bytes =
+      bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
+  const size_t off_tables = 0, off_derived = tables_bytes, off_am = off_derived + align256(tab_plan.end()),
+               off_image = off_am + align256(am_bytes);
+
+  // ---- enumeration / unwind descriptors (pointer-free parts) ----------------
+  std::vector<int> pos(static_cast<size_t>(t.nl), -1);
+  int64_t space = 1;
+  std::vector<int32_t> node_layer(static_cast<size_t>(K));
+  for (int d = 0; d < K; ++d) {
+    const int l = s.final_nodes[static_cast<size_t>(d)];
+    node_layer[static_cast<size_t>(d)] = l;
+    pos[static_cast<size_t>(l)] = d;
+    PP_REQUIRE(space <= INT64_MAX / std::max(1, t.counts[static_cast<size_t>(l)]), "final enumeration space overflows");
+    space *= t.counts[static_cast<size_t>(l)];
+  }
+  const int64_t lanes = int64_t(ctx->sms) * 8 * kEnumThreads;
+  const int64_t per_thread = std::max<int64_t>(1, (space + lanes - 1) / lanes);
+  const int nblk = static_cast<int>(((space + per_thread - 1) / per_thread + kEnumThreads - 1) / kEnumThreads);
+  std::vector<int32_t> es(t.esrc.begin(), t.esrc.end()), ed(t.edst.begin(), t.edst.end());
+  using A = typename Acc<T>::type;
+
+  // ---- descriptor image, as a function of the device base --------------------
+  struct WaveRange {
+    size_t f0, m0;
+    int nf, nm;
+    int64_t ftiles, mblocks;
+    double cells;
+  };
+  struct Image {
+    Packer pk;
+    std::vector<WaveRange> waves;
+    size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw;
+    size_t res_bytes;
+  };
+  auto make_image = [&](unsigned char *db) {
+    Image im;
+    auto tabp = [&](int id) -> const T * {
+      if (id < t.ne) {
+        const T *ox = bp ? reinterpret_cast<const T *>(db + off_tables + 3 * align256(static_cast<size_t>(t.ncells) * 8))
+                         : (t.mode == kFP64 ? reinterpret_cast<const T *>(t.xfer64.p)
+                                            : reinterpret_cast<const T *>(t.xfer32.p));
+        return ox + t.xoff[static_cast<size_t>(id)];
+      }
+      return reinterpret_cast<const T *>(db + off_derived + tab_off[static_cast<size_t>(id)]);
+    };
+    const T *onode = bp ? reinterpret_cast<const T *>(db + off_tables)
+                        : (t.mode == kFP64 ? reinterpret_cast<const T *>(t.node.p)
+                                           : reinterpret_cast<const T *>(t.node32.p));
+    std::vector<FoldDesc<T>> folds;
+    std::vector<MergeDesc<T>> merges;
+    for (int w = 1; w <= s.n_waves; ++w) {
+      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0};
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        T *out = const_cast<T *>(tabp(op.ne));
+        if (!op.type) {
+          FoldDesc<T> f;
+          f.t1 = tabp(op.e1);
+          f.t2 = tabp(op.e2);
+          f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
+          f.out = out;
+          f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
+          f.nu = rows[static_cast<size_t>(op.e1)];
+          f.nw = t.counts[static_cast<size_t>(op.removed)];
+          f.nv = cols[static_cast<size_t>(op.e2)];
+          f.tiles_k = (f.nv + kTile - 1) / kTile;
+          f.tile_begin = wr.ftiles;
+          wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
+          wr.ftiles += static_cast<int64_t>((f.nu + kTile - 1) / kTile) * f.tiles_k;
+          folds.push_back(f);
+          ++wr.nf;
+        } else {
+          MergeDesc<T> m;
+          m.a = tabp(op.e1);
+          m.b = tabp(op.e2);
+          m.out = out;
+          m.n = static_cast<int64_t>(cells(op.ne));
+          m.blk_begin = wr.mblocks;
+          wr.cells += static_cast<double>(m.n);
+          wr.mblocks += (m.n + kMergePerBlock - 1) / kMergePerBlock;
+          merges.push_back(m);
+          ++wr.nm;
+        }
+      }
+      im.waves.push_back(wr);
+    }
+    std::vector<EnumNode> en(static_cast<size_t>(K));
+    for (int d = 0; d < K; ++d) {
+      const int l = node_layer[static_cast<size_t>(d)];
+      en[static_cast<size_t>(d)] = EnumNode{onode + t.cat_off[static_cast<size_t>(l)], t.counts[static_cast<size_t>(l)], 0};
+    }
+    std::vector<EnumEdge> ee;
+    for (int id : s.final_edges)
+      ee.push_back(EnumEdge{tabp(id), pos[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])],
+                            pos[static_cast<size_t>(s.edst[static_cast<size_t>(id)])], cols[static_cast<size_t>(id)], 0});
+    std::vector<UnwindRec> recs;
+    for (size_t oi = 0; oi < s.ops.size(); ++oi) {
+      const Op &op = s.ops[oi];
+      if (op.type) continue;
+      recs.push_back(UnwindRec{reinterpret_cast<const uint16_t *>(db + off_am + am_off[oi]), op.removed, op.u, op.v,
+                               cols[static_cast<size_t>(op.ne)]});
+    }
+    Packer &pk = im.pk;
+    im.oF = pk.put(folds);
+    im.oM = pk.put(merges);
+    im.oN = pk.put(en);
+    im.oE = pk.put(ee);
+    im.oR = pk.put(recs);
+    im.oL = pk.put(node_layer);
+    im.oCO = pk.put(t.cat_off);
+    im.oXO = pk.put(t.xoff);
+    im.oS = pk.put(es);
+    im.oD = pk.put(ed);
+    im.oC = pk.put(t.counts);
+    if (bp) {
+      im.oLay = pk.put(bp->L);
+      im.oEdg = pk.put(bp->E);
+      im.oCfg = pk.put(t.configs);
+      im.oRat = pk.put(bp->rates);
+      im.oBw = pk.put(bp->bw);
+    }
+    im.oBV = pk.put(std::vector<A>(static_cast<size_t>(nblk)));
+    im.oBI = pk.put(std::vector<int64_t>(static_cast<size_t>(nblk)));
+    // result slots, contiguous: indices[nl] | digits[K] | final_cost | cost
+    im.oRes = pk.put(std::vector<int32_t>(static_cast<size_t>(t.nl) + static_cast<size_t>(K) + 2));
+    im.oIdx = im.oRes;
+    im.oFC = pk.put(std::vector<double>(2));
+    im.res_bytes = im.oFC + 16 - im.oRes;
+    return im;
+  };
+
+  // sizes (pointer values do not change the layout)
+  const size_t image_bytes = make_image(nullptr).pk.size();
+  const size_t total = off_image + align256(image_bytes);
+  if (P->transient) {
+    ctx->plan_pool.ensure(total);
+    P->dbase = ctx->plan_pool.p;
+    P->hbase = static_cast<unsigned char *>(ctx->plan_pinned.ensure(align256(image_bytes)));
+  } else {
+    P->dmem.alloc(total);
+    P->dbase = P->dmem.p;
+    P->hbase = static_cast<unsigned char *>(P->hmem.ensure(align256(image_bytes)));
+  }
+  unsigned char *db = P->dbase;
+  unsigned char *dimg = db + off_image;
+  Image im = make_image(db);
+  std::memcpy(P->hbase, im.pk.bytes.data(), im.pk.size());
+  P->image_off = off_image;
+  P->image_bytes = im.pk.size();
+  P->res_off = im.oRes;
+  P->res_bytes = im.res_bytes;
+  P->off_idx = im.oIdx;
+  P->off_cost = im.oFC;
+
+  if (bp) { // tables live in the plan's memory
+    t.node.view(db + off_tables, static_cast<size_t>(t.ncells));
+    t.compute.view(db + off_tables + align256(static_cast<size_t>(t.ncells) * 8), static_cast<size_t>(t.ncells));
+    t.sync.view(db + off_tables + 2 * align256(static_cast<size_t>(t.ncells) * 8), static_cast<size_t>(t.ncells));
+    t.xfer64.view(db + off_tables + 3 * align256(static_cast<size_t>(t.ncells) * 8), static_cast<size_t>(t.xcells));
+  }
+
+  // ---- launch steps -------------------------------------------------------------
+  P->steps.clear();
+  P->step_kind.clear();
+  P->step_work.clear();
+  int launches = 0;
+  if (bp && bp->grid > 0) {
+    BuildArgs a;
+    a.layers = reinterpret_cast<const LayerDev *>(dimg + im.oLay);
+    a.edges = reinterpret_cast<const EdgeDev *>(dimg + im.oEdg);
+    a.cfg = reinterpret_cast<const int64_t *>(dimg + im.oCfg);
+    a.rates = reinterpret_cast<const double *>(dimg + im.oRat);
+    a.bw = reinterpret_cast<const double *>(dimg + im.oBw);
+    a.node = t.node.p, a.compute = t.compute.p, a.sync = t.sync.p, a.xfer = t.xfer64.p;
+    a.ncells = t.ncells;
+    a.nl = t.nl, a.ne = t.ne, a.D = bp->D;
+    a.node_blocks = static_cast<int32_t>(bp->node_blocks);
+    a.bw_uniform = bp->bw_uniform;
+    const int64_t grid = bp->grid;
+    P->steps.push_back([ctx, a, grid](cudaStream_t) { launch_build(ctx, a, grid); });
+    P->step_kind.push_back(0);
+    P->step_work.push_back(static_cast<double>(t.ncells + t.xcells));
+    ++launches;
+  }
+  for (const auto &wr : im.waves) {
+    const int64_t grid = wr.ftiles + wr.mblocks;
+    if (!grid) continue;
+    PP_REQUIRE(grid < (int64_t(1) << 31), "wave too large for one launch");
+    const FoldDesc<T> *f = reinterpret_cast<const FoldDesc<T> *>(dimg + im.oF) + wr.f0;
+    const MergeDesc<T> *m = reinterpret_cast<const MergeDesc<T> *>(dimg + im.oM) + wr.m0;
+    const int nf = wr.nf, nm = wr.nm;
+    const int64_t ft = wr.ftiles;
+    P->steps.push_back([ctx, f, nf, ft, m, nm, grid](cudaStream_t st) {
+      wave_kernel<T><<<static_cast<unsigned>(grid), kFoldThreads, 0, st>>>(f, nf, ft, m, nm);
+      check_launch(ctx);
+    });
+    P->step_kind.push_back(1);
+    P->step_work.push_back(wr.cells);
+    ++launches;
+  }
+  {
+    const EnumNode *en = reinterpret_cast<const EnumNode *>(dimg + im.oN);
+    const EnumEdge *ee = reinterpret_cast<const EnumEdge *>(dimg + im.oE);
+    const int m = static_cast<int>(s.final_edges.size());
+    A *bv = reinterpret_cast<A *>(dimg + im.oBV);
+    int64_t *bi = reinterpret_cast<int64_t *>(dimg + im.oBI);
+    P->steps.push_back([ctx, en, K, ee, m, space, per_thread, bv, bi, nblk](cudaStream_t st) {
+      enum_kernel<T><<<nblk, kEnumThreads, 0, st>>>(en, K, ee, m, space, per_thread, bv, bi);
+      check_launch(ctx);
+    });
+    P->step_kind.push_back(2);
+    P->step_work.push_back(static_cast<double>(space));
+    FinishArgs fa{};
+    fa.blk_val = bv;
+    fa.blk_idx = bi;
+    fa.nblk = nblk;
+    fa.nodes = en;
+    fa.k = K;
+    fa.node_layer = reinterpret_cast<const int32_t *>(dimg + im.oL);
+    fa.indices = reinterpret_cast<int32_t *>(dimg + im.oIdx);
+    fa.digits = fa.indices + t.nl;
+    fa.final_cost = reinterpret_cast<double *>(dimg + im.oFC);
+    fa.cost = fa.final_cost + 1;
+    fa.shift = t.shift;
+    fa.recs = reinterpret_cast<const UnwindRec *>(dimg + im.oR);
+    fa.n_rec = static_cast<int>(s.node_ops);
+    fa.nl = t.nl;
+    fa.onode = bp ? static_cast<const void *>(t.node.p)
+                  : (t.mode == kFP64 ? static_cast<const void *>(t.node.p) : static_cast<const void *>(t.node32.p));
+    fa.oxfer = bp ? static_cast<const void *>(t.xfer64.p)
+                  : (t.mode == kFP64 ? static_cast<const void *>(t.xfer64.p) : static_cast<const void *>(t.xfer32.p));
+    fa.cat_off = reinterpret_cast<const int64_t *>(dimg + im.oCO);
+    fa.xoff = reinterpret_cast<const int64_t *>(dimg + im.oXO);
+    fa.esrc = reinterpret_cast<const int32_t *>(dimg + im.oS);
+    fa.edst = reinterpret_cast<const int32_t *>(dimg + im.oD);
+    fa.counts = reinterpret_cast<const int32_t *>(dimg + im.oC);
+    fa.ne = t.ne;
+    P->steps.push_back([ctx, fa](cudaStream_t st) {
+      finish_kernel<T><<<1, 32, 0, st>>>(fa);
+      check_launch(ctx);
+    });
+    P->step_kind.push_back(3);
+    P->step_work.push_back(0.0);
+    launches += 2;
+  }
+  unsigned char *hres = P->hbase + P->res_off, *dres = dimg + P->res_off;
+  const size_t rb = P->res_bytes;
+  P->steps.push_back([hres, dres, rb](cudaStream_t st) {
+    PP_CUDA(cudaMemcpyAsync(hres, dres, rb, cudaMemcpyDeviceToHost, st));
+  });
+  P->step_kind.push_back(4);
+  P->step_work.push_back(static_cast<double>(rb));
+  P->launches_per_run = launches;
+}
+
+static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
+  BuildPlan bp;
+  if (dev) {
+    P->own_t = std::make_unique<Tables>();
+    P->t = P->own_t.get();
+    P->t->ctx = P->ctx;
+    bp = plan_build(*P->t, *P->g, dev);
+    bp.rates.assign(dev->compute_rates, dev->compute_rates + dev->count);
+    bp.bw.assign(dev->bandwidth, dev->bandwidth + static_cast<size_t>(dev->count) * dev->count);
+  }
+  PP_REQUIRE(P->t->nl == P->g->nl && P->t->ne == P->g->ne, "tables do not match the graph");
+  if (P->t->mode == kFP64)
+    build_steps<double>(P, dev ? &bp : nullptr, k_bound);
+  else
+    build_steps<int32_t>(P, dev ? &bp : nullptr, k_bound);
+}
+
+static void launch(pp_prepared *P, bool upload) {
+  pp_context *ctx = P->ctx;
+  ctx->begin();
+  if (upload || !P->uploaded) {
+    PP_CUDA(cudaMemcpyAsync(P->dbase + P->image_off, P->hbase, P->image_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    P->uploaded = true;
+  }
+  if (P->exec) {
+    PP_CUDA(cudaGraphLaunch(P->exec, ctx->stream));
+    ctx->launches += P->launches_per_run;
+  } else {
+    for (auto &st : P->steps) st(ctx->stream);
+  }
+  PP_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  P->launched = true;
+}
+
+static void fetch(pp_prepared *P, int32_t *indices, pp_plan_result *res) {
+  PP_REQUIRE(P->launched, "plan was not launched");
+  pp_context *ctx = P->ctx;
+  PP_CUDA(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  PP_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  const unsigned char *h = P->hbase + P->res_off;
+  if (indices) std::memcpy(indices, h, static_cast<size_t>(P->t->nl) * 4);
+  double fc[2];
+  std::memcpy(fc, P->hbase + P->off_cost, 16);
+  if (res) {
+    res->cost = fc[1];
+    res->final_graph_nodes = P->K;
+    res->node_eliminations = P->node_ops;
+    res->edge_eliminations = P->edge_ops;
+    res->precision = P->t->mode;
+    res->waves = P->n_waves;
+    res->launches = P->launches_per_run;
+    res->device_ms = ms;
+    res->h2d_bytes = static_cast<int64_t>(P->image_bytes);
+    res->d2h_bytes = static_cast<int64_t>(P->res_bytes);
+  }
+}
+
+void run_plan(pp_context *ctx, Graph &g, Tables *t, const pp_device_desc *dev, int k_bound, int32_t *indices,
+              pp_plan_result *res) {
+  pp_prepared P;
+  P.ctx = ctx;
+  P.g = &g;
+  P.t = t;
+  P.transient = true;
+  PP_CUDA(cudaSetDevice(ctx->device));
+  prepare(&P, dev, k_bound);
+  launch(&P, true);
+  fetch(&P, indices, res);
+}
+
+} // namespace pp
+
+extern "C" {
+
+pp_status pp_plan_with_tables(pp_context *ctx, const pp_graph *g, pp_tables *t, int32_t k_bound, int32_t *indices,
+                              pp_plan_result *res) {
+  return guard([&] {
+    PP_REQUIRE(ctx && g && t && indices, "pp_plan_with_tables: null argument");
+    run_plan(ctx, const_cast<pp_graph *>(g)->impl, &t->impl, nullptr, k_bound, indices, res);
+  });
+}
+
+pp_status pp_plan(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev, int32_t k_bound, int32_t *indices,
+                  pp_plan_result *res) {
+  return guard([&] {
+    PP_REQUIRE(ctx && g && dev && indices, "pp_plan: null argument");
+    run_plan(ctx, const_cast<pp_graph *>(g)->impl, nullptr, dev, k_bound, indices, res);
+  });
+}
+
+pp_status pp_plan_prepare(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev, pp_tables *t, int32_t k_bound,
+                          pp_prepared **out) {
+  return guard([&] {
+    PP_REQUIRE(ctx && g && out && (dev != nullptr) != (t != nullptr), "pp_plan_prepare: give exactly one of dev, t");
+    auto P = std::make_unique<pp_prepared>();
+    P->ctx = ctx;
+    P->g = &const_cast<pp_graph *>(g)->impl;
+    P->t = t ? &t->impl : nullptr;
+    P->transient = false;
+    PP_CUDA(cudaSetDevice(ctx->device));
+    prepare(P.get(), dev, k_bound);
+    // capture the device work as one CUDA graph
+    PP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = ctx->launches;
+    for (auto &st : P->steps) st(ctx->stream);
+    ctx->launches = l0;
+    PP_CUDA(cudaStreamEndCapture(ctx->stream, &P->graph));
+    PP_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
+    *out = P.release();
+  });
+}
+
+pp_status pp_plan_launch(pp_prepared *P, int32_t upload_inputs) {
+  return guard([&] {
+    PP_REQUIRE(P, "null plan");
+    launch(P, upload_inputs != 0);
+  });
+}
+
+pp_status pp_plan_fetch(pp_prepared *P, int32_t *indices, pp_plan_result *res) {
+  return guard([&] {
+    PP_REQUIRE(P, "null plan");
+    fetch(P, indices, res);
+  });
+}
+
+pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t *step_kind, double *step_work,
+                          int32_t *n_steps) {
+  return guard([&] {
+    PP_REQUIRE(P && n_steps, "null argument");
+    pp_context *ctx = P->ctx;
+    const int n = static_cast<int>(P->steps.size());
+    *n_steps = n;
+    if (!step_ms || cap <= 0) return;
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(n) + 1);
+    for (auto &e : ev) PP_CUDA(cudaEventCreate(&e));
+    PP_CUDA(cudaSetDevice(ctx->device));
+    if (!P->uploaded) {
+      PP_CUDA(cudaMemcpyAsync(P->dbase + P->image_off, P->hbase, P->image_bytes, cudaMemcpyHostToDevice, ctx->stream));
+      P->uploaded = true;
+    }
+    PP_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    for (int k = 0; k < n; ++k) {
+      P->steps[static_cast<size_t>(k)](ctx->stream);
+      PP_CUDA(cudaEventRecord(ev[static_cast<size_t>(k) + 1], ctx->stream));
+    }
+    PP_CUDA(cudaEventSynchronize(ev.back()));
+    for (int k = 0; k < n && k < cap; ++k) {
+      float ms = 0.f;
+      PP_CUDA(cudaEventElapsedTime(&ms, ev[static_cast<size_t>(k)], ev[static_cast<size_t>(k) + 1]));
+      step_ms[k] = ms;
+      if (step_kind) step_kind[k] = P->step_kind[static_cast<size_t>(k)];
+      if (step_work) step_work[k] = P->step_work[static_cast<size_t>(k)];
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+  });
+}
+
+pp_status pp_plan_destroy(pp_prepared *P) {
+  if (P && P->ctx) {
+    cudaSetDevice(P->ctx->device);
+    cudaStreamSynchronize(P->ctx->stream);
+  }
+  delete P;
+  return PP_OK;
+}
+
+} // extern "C"

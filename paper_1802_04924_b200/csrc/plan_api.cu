@@ -58,33 +58,6 @@ void apply(pp_reduced *rg, const Op &op) {
 
 extern "C" {
 
-pp_status pp_plan_with_tables(pp_context *ctx, const pp_graph *g, pp_tables *t, int32_t k_bound, int32_t *indices,
-                              pp_plan_result *res) {
-  return guard([&] {
-    PP_REQUIRE(ctx && g && t && indices, "pp_plan_with_tables: null argument");
-    run_plan(ctx, const_cast<pp_graph *>(g)->impl, t->impl, k_bound, indices, res);
-  });
-}
-
-pp_status pp_plan(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev, int32_t k_bound, int32_t *indices,
-                  pp_plan_result *res) {
-  pp_tables *t = nullptr;
-  pp_status st = pp_tables_build(ctx, g, dev, &t);
-  if (st != PP_OK) return st;
-  st = guard([&] {
-    PP_REQUIRE(indices, "pp_plan: null indices");
-    run_plan(ctx, const_cast<pp_graph *>(g)->impl, t->impl, k_bound, indices, res);
-    if (res) {
-      res->device_ms += t->impl.build_ms;
-      res->launches += 1;
-    }
-  });
-  const std::string err = pp_last_error();
-  pp_tables_destroy(t);
-  if (st != PP_OK) pp::set_last_error(err);
-  return st;
-}
-
 pp_status pp_reduced_create(pp_context *ctx, const pp_graph *g, pp_tables *t, pp_reduced **out) {
   return guard([&] {
     PP_REQUIRE(ctx && g && t && out, "pp_reduced_create: null argument");

@@ -92,15 +92,34 @@ pp_status pp_context_create(int32_t device, pp_context **out) {
   });
 }
 
+pp_status pp_context_create_on_stream(int32_t device, void *stream, pp_context **out) {
+  pp_context *ctx = nullptr;
+  pp_status st = pp_context_create(device, &ctx);
+  if (st != PP_OK) return st;
+  cudaStreamDestroy(ctx->stream);
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  ctx->external_stream = true;
+  *out = ctx;
+  return PP_OK;
+}
+
+pp_status pp_context_stream(const pp_context *ctx, void **stream) {
+  return guard([&] {
+    PP_REQUIRE(ctx && stream, "null argument");
+    *stream = ctx->stream;
+  });
+}
+
 pp_status pp_context_destroy(pp_context *ctx) {
   if (!ctx) return PP_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->desc.release();
   ctx->scratch.release();
+  ctx->plan_pool.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream && !ctx->external_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PP_OK;
 }
@@ -127,42 +146,6 @@ pp_status pp_context_launch_count(const pp_context *ctx, int64_t *n) {
 // ---------------------------------------------------------------------------
 
 namespace pp {
-
-struct LayerDev {
-  int64_t shape[4];
-  int64_t in_shape[4];
-  int64_t params[7];
-  int64_t cat_off;
-  int32_t kind;
-  int32_t count;
-};
-
-struct EdgeDev {
-  int64_t sshape[4];
-  int64_t dshape[4];
-  int64_t params[7];
-  int64_t band;
-  int64_t cat_u, cat_v;
-  int64_t out_off;
-  int64_t cells;
-  int64_t blk_begin;
-  int32_t kind;
-  int32_t nu, nv;
-  int32_t pad;
-};
-
-struct BuildArgs {
-  const LayerDev *layers;
-  const EdgeDev *edges;
-  const int64_t *cfg; // 4 per config
-  const double *rates;
-  const double *bw; // D*D
-  double *node, *compute, *sync, *xfer;
-  int64_t ncells;
-  int32_t nl, ne, D;
-  int32_t node_blocks;
-  double bw_uniform; // > 0 when every off-diagonal bandwidth is this value
-};
 
 constexpr int kBuildThreads = 128;
 
@@ -395,22 +378,62 @@ extern "C" {
 pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_desc *dev, pp_tables **out) {
   return guard([&] {
     PP_REQUIRE(ctx && gh && dev && out, "pp_tables_build: null argument");
-    const Graph &g = gh->impl;
-    const int D = dev->count;
-    // DeviceGraph validation (graph.hpp:193-214)
-    const parplan::DeviceGraph dg(std::vector<double>(dev->compute_rates, dev->compute_rates + D),
-                                  std::vector<double>(dev->bandwidth, dev->bandwidth + static_cast<size_t>(D) * D));
-    if (D < 1) throw parplan::InputError("device graph: need at least one device");
     auto tp = std::make_unique<pp_tables>();
     Tables &t = tp->impl;
     t.ctx = ctx;
-    std::vector<int32_t> counts;
-    enumerate_catalogs(g, D, &counts, &t.configs);
-    init_layout(t, g, counts);
-    t.mode = kFP64;
-    t.analytic = true;
+    const BuildPlan bp = plan_build(t, gh->impl, dev);
+    Packer pk;
+    const size_t oL = pk.put(bp.L), oE = pk.put(bp.E), oC = pk.put(t.configs);
+    const size_t oR = pk.put(dev->compute_rates, static_cast<size_t>(bp.D));
+    const size_t oB = pk.put(dev->bandwidth, static_cast<size_t>(bp.D) * bp.D);
+    t.node.alloc(static_cast<size_t>(t.ncells));
+    t.compute.alloc(static_cast<size_t>(t.ncells));
+    t.sync.alloc(static_cast<size_t>(t.ncells));
+    t.xfer64.alloc(static_cast<size_t>(t.xcells));
+    ctx->begin();
+    unsigned char *base = ctx->upload(pk);
+    BuildArgs a;
+    a.layers = reinterpret_cast<const LayerDev *>(base + oL);
+    a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
+    a.cfg = reinterpret_cast<const int64_t *>(base + oC);
+    a.rates = reinterpret_cast<const double *>(base + oR);
+    a.bw = reinterpret_cast<const double *>(base + oB);
+    a.node = t.node.p, a.compute = t.compute.p, a.sync = t.sync.p, a.xfer = t.xfer64.p;
+    a.ncells = t.ncells;
+    a.nl = t.nl, a.ne = t.ne, a.D = bp.D;
+    a.node_blocks = static_cast<int32_t>(bp.node_blocks);
+    a.bw_uniform = bp.bw_uniform;
+    launch_build(ctx, a, bp.grid);
+    t.build_ms = ctx->end_ms();
+    *out = tp.release();
+  });
+}
 
-    double bw_uniform = dev->bandwidth[D > 1 ? 1 : 0];
+} // extern "C"
+
+namespace pp {
+
+void launch_build(pp_context *ctx, const BuildArgs &a, int64_t grid) {
+  if (grid <= 0) return;
+  build_tables_kernel<<<static_cast<unsigned>(grid), kBuildThreads, 0, ctx->stream>>>(a);
+  check_launch(ctx);
+}
+
+BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev) {
+  const int D = dev->count;
+  if (D < 1) throw parplan::InputError("device graph: need at least one device");
+  // DeviceGraph validation (graph.hpp:193-214)
+  const parplan::DeviceGraph dg(std::vector<double>(dev->compute_rates, dev->compute_rates + D),
+                                std::vector<double>(dev->bandwidth, dev->bandwidth + static_cast<size_t>(D) * D));
+  std::vector<int32_t> counts;
+  enumerate_catalogs(g, D, &counts, &t.configs);
+  init_layout(t, g, counts);
+  t.mode = kFP64;
+  t.analytic = true;
+  BuildPlan bp;
+  bp.D = D;
+
+  double bw_uniform = dev->bandwidth[D > 1 ? 1 : 0];
     for (int p = 0; p < D; ++p)
       for (int q = 0; q < D; ++q)
         if (p != q && dev->bandwidth[static_cast<size_t>(p) * D + q] != bw_uniform) bw_uniform = -1.0;
@@ -449,39 +472,17 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
     }
     const int64_t node_blocks = (t.ncells + kBuildThreads - 1) / kBuildThreads;
     PP_REQUIRE(node_blocks + blocks < (int64_t(1) << 31), "cost tables too large for one launch");
-
-    Packer pk;
-    const size_t oL = pk.put(L), oE = pk.put(E), oC = pk.put(t.configs);
-    const size_t oR = pk.put(dev->compute_rates, static_cast<size_t>(D));
-    const size_t oB = pk.put(dev->bandwidth, static_cast<size_t>(D) * D);
-
-    t.node.alloc(static_cast<size_t>(t.ncells));
-    t.compute.alloc(static_cast<size_t>(t.ncells));
-    t.sync.alloc(static_cast<size_t>(t.ncells));
-    t.xfer64.alloc(static_cast<size_t>(t.xcells));
-
-    ctx->begin();
-    unsigned char *base = ctx->upload(pk);
-    BuildArgs a;
-    a.layers = reinterpret_cast<const LayerDev *>(base + oL);
-    a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
-    a.cfg = reinterpret_cast<const int64_t *>(base + oC);
-    a.rates = reinterpret_cast<const double *>(base + oR);
-    a.bw = reinterpret_cast<const double *>(base + oB);
-    a.node = t.node.p, a.compute = t.compute.p, a.sync = t.sync.p, a.xfer = t.xfer64.p;
-    a.ncells = t.ncells;
-    a.nl = g.nl, a.ne = g.ne, a.D = D;
-    a.node_blocks = static_cast<int32_t>(node_blocks);
-    a.bw_uniform = bw_uniform;
-    const int64_t grid = node_blocks + blocks;
-    if (grid > 0) {
-      build_tables_kernel<<<static_cast<unsigned>(grid), kBuildThreads, 0, ctx->stream>>>(a);
-      check_launch(ctx);
-    }
-    t.build_ms = ctx->end_ms();
-    *out = tp.release();
-  });
+    bp.L = std::move(L);
+    bp.E = std::move(E);
+    bp.node_blocks = node_blocks;
+    bp.grid = node_blocks + blocks;
+    bp.bw_uniform = bw_uniform;
+    return bp;
 }
+
+} // namespace pp
+
+extern "C" {
 
 pp_status pp_tables_upload(pp_context *ctx, const pp_graph *gh, const int32_t *counts, const int64_t *configs,
                            const double *node, const double *xfer, pp_tables **out) {

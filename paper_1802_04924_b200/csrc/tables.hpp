@@ -35,6 +35,58 @@ struct Tables {
   int64_t xfer_bytes() const { return xcells * (mode == kFP64 ? 8 : 4); }
 };
 
+// ---- K1/K2 launch descriptors ------------------------------------------------
+
+struct LayerDev {
+  int64_t shape[4];
+  int64_t in_shape[4];
+  int64_t params[7];
+  int64_t cat_off;
+  int32_t kind;
+  int32_t count;
+};
+
+struct EdgeDev {
+  int64_t sshape[4];
+  int64_t dshape[4];
+  int64_t params[7];
+  int64_t band;
+  int64_t cat_u, cat_v;
+  int64_t out_off;
+  int64_t cells;
+  int64_t blk_begin;
+  int32_t kind;
+  int32_t nu, nv;
+  int32_t pad;
+};
+
+struct BuildArgs {
+  const LayerDev *layers;
+  const EdgeDev *edges;
+  const int64_t *cfg; // 4 per config
+  const double *rates;
+  const double *bw; // D*D
+  double *node, *compute, *sync, *xfer;
+  int64_t ncells;
+  int32_t nl, ne, D;
+  int32_t node_blocks;
+  double bw_uniform; // > 0 when every off-diagonal bandwidth is this value
+};
+
+struct BuildPlan {
+  std::vector<LayerDev> L;
+  std::vector<EdgeDev> E;
+  int64_t node_blocks = 0, grid = 0;
+  double bw_uniform = 0.0;
+  int D = 0;
+  std::vector<double> rates, bw; // the device graph, for plans that embed it
+};
+
+// Fills t's layout (catalogs, offsets; FP64 analytic mode, no allocation) and
+// the K1/K2 launch descriptors for graph g on devices dev.
+BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev);
+void launch_build(pp_context *ctx, const BuildArgs &a, int64_t grid);
+
 // Decides fixed point vs FP64 for host tables and fills the span bounds.
 // Returns true when every value is k * 2^-s (s <= 24) and every possible sum
 // of one entry per table stays below 2^31 units (the exactness certificate).
