@@ -171,7 +171,8 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # planner and timing events share this stream
+    torch.cuda.set_stream(stream)
     ctx = P.Context(local, stream=stream.cuda_stream)
     model, batch, D = workload(args.workload)
     g = P.builtin_model(model if model != "inception_chain" else "inception_chain", batch)

@@ -26,6 +26,9 @@ from .capi import (  # noqa: F401
     lib,
     plan,
     plan_with_tables,
+    random_series_parallel_graph,
+    series_parallel_graph,
+    synthetic_instance,
     synthetic_cost_tables,
     upload_cost_tables,
 )

@@ -284,6 +284,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   } else {
     P->dmem.alloc(total);
     P->dbase = P->dmem.p;
+    // poison: a slot the device work fails to write shows up as garbage
+    PP_CUDA(cudaMemsetAsync(P->dbase, 0xFF, total, ctx->stream));
     P->hbase = static_cast<unsigned char *>(P->hmem.ensure(align256(image_bytes)));
   }
   unsigned char *db = P->dbase;
@@ -322,7 +324,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     a.node_blocks = static_cast<int32_t>(bp->node_blocks);
     a.bw_uniform = bp->bw_uniform;
     const int64_t grid = bp->grid;
-    P->steps.push_back([ctx, a, grid](cudaStream_t) { launch_build(ctx, a, grid); });
+    P->steps.push_back([ctx, a, grid](cudaStream_t st) { launch_build(ctx, st, a, grid); });
     P->step_kind.push_back(0);
     P->step_work.push_back(static_cast<double>(t.ncells + t.xcells));
     ++launches;
@@ -500,12 +502,27 @@ pp_status pp_plan_prepare(pp_context *ctx, const pp_graph *g, const pp_device_de
     P->transient = false;
     PP_CUDA(cudaSetDevice(ctx->device));
     prepare(P.get(), dev, k_bound);
-    // capture the device work as one CUDA graph
-    PP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    // capture the device work as one CUDA graph, on a private stream (the
+    // context stream may be the legacy default stream, which cannot capture);
+    // the graph is launched on the context stream
+    cudaStream_t cap = nullptr;
+    PP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     const int64_t l0 = ctx->launches;
-    for (auto &st : P->steps) st(ctx->stream);
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      try {
+        for (auto &st : P->steps) st(cap);
+      } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(cap, &dummy);
+        cudaStreamDestroy(cap);
+        throw;
+      }
+      e = cudaStreamEndCapture(cap, &P->graph);
+    }
     ctx->launches = l0;
-    PP_CUDA(cudaStreamEndCapture(ctx->stream, &P->graph));
+    cudaStreamDestroy(cap);
+    PP_CUDA(e);
     PP_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
     *out = P.release();
   });

@@ -403,7 +403,7 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
     a.nl = t.nl, a.ne = t.ne, a.D = bp.D;
     a.node_blocks = static_cast<int32_t>(bp.node_blocks);
     a.bw_uniform = bp.bw_uniform;
-    launch_build(ctx, a, bp.grid);
+    launch_build(ctx, ctx->stream, a, bp.grid);
     t.build_ms = ctx->end_ms();
     *out = tp.release();
   });
@@ -413,9 +413,9 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
 
 namespace pp {
 
-void launch_build(pp_context *ctx, const BuildArgs &a, int64_t grid) {
+void launch_build(pp_context *ctx, cudaStream_t st, const BuildArgs &a, int64_t grid) {
   if (grid <= 0) return;
-  build_tables_kernel<<<static_cast<unsigned>(grid), kBuildThreads, 0, ctx->stream>>>(a);
+  build_tables_kernel<<<static_cast<unsigned>(grid), kBuildThreads, 0, st>>>(a);
   check_launch(ctx);
 }
 

@@ -85,7 +85,7 @@ struct BuildPlan {
 // Fills t's layout (catalogs, offsets; FP64 analytic mode, no allocation) and
 // the K1/K2 launch descriptors for graph g on devices dev.
 BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev);
-void launch_build(pp_context *ctx, const BuildArgs &a, int64_t grid);
+void launch_build(pp_context *ctx, cudaStream_t st, const BuildArgs &a, int64_t grid);
 
 // Decides fixed point vs FP64 for host tables and fills the span bounds.
 // Returns true when every value is k * 2^-s (s <= 24) and every possible sum

@@ -1,0 +1,59 @@
+"""CUDA path vs fixtures generated from the REAL reference (tests/golden/
+make_golden.py via oracle/_ref) — including the sizes the CPU oracle is too
+slow for in a test: Inception-chain(12)@64 (reference: ~2 min) and the
+config-5 synthetic graph at C=256 (reference: ~45 s)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
+
+
+def sha(arrs):
+    h = hashlib.sha256()
+    for a in arrs:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("case", GOLD["builtins"], ids=lambda c: f"{c['model']}@{c['devices']}")
+def test_builtin_golden(gpu, case):
+    import paper_1802_04924_b200 as P
+
+    g = P.builtin_model(case["model"], case["batch"])
+    dev = P.DeviceGraph.uniform(case["devices"])
+    t = P.build_cost_tables(g, dev, gpu.ctx)
+    cat, node, comp, sync, xfer = t.download()
+    assert [len(c) for c in cat] == case["config_counts"]
+    assert sha(node) == case["node_sha256"]
+    assert sha(comp) == case["compute_sha256"]
+    assert sha(sync) == case["sync_sha256"]
+    assert [sha([x]) for x in xfer] == case["xfer_sha256"]
+    r = P.plan(g, dev, ctx=gpu.ctx)
+    assert [int(x) for x in r.indices] == case["indices"]
+    assert float(r.cost).hex() == case["cost"]
+    assert [r.final_graph_nodes, r.node_eliminations, r.edge_eliminations] == case["stats"]
+    sched, _ = g.schedule()
+    assert [list(s[:7]) for s in sched] == case["log"]
+    if sum(case["config_counts"]) < 5000:
+        rg = P.ReducedGraph(g, t)
+        rg.reduce()
+        am = [sha([rg.argmin(i).astype(np.int32)]) for i, rec in enumerate(rg.log()) if rec[0] == 0]
+        assert am == case["argmin_sha256"]
+
+
+@pytest.mark.parametrize("case", GOLD["synthetic"], ids=lambda c: f"C{c['configs']}")
+def test_synthetic_golden(gpu, case):
+    import paper_1802_04924_b200 as P
+
+    g, t = P.synthetic_instance(case["seed"], case["nodes"], case["configs"], case["bp"], ctx=gpu.ctx)
+    r = P.plan_with_tables(g, t)
+    assert r.precision == "fixed"
+    assert [int(x) for x in r.indices] == case["indices"]
+    assert float(r.cost).hex() == case["cost"]
+    assert [r.final_graph_nodes, r.node_eliminations, r.edge_eliminations] == case["stats"]

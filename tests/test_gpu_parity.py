@@ -96,3 +96,53 @@ def test_fp64_and_fixed_point_agree(gpu):
     b = P.plan_with_tables(g, t_64)
     assert a.precision == "fixed" and b.precision == "fp64"
     assert list(a.indices) == list(b.indices) and a.cost == b.cost == inst.plan().cost
+
+
+def test_prepared_plan_and_profile(gpu):
+    import paper_1802_04924_b200 as P
+
+    g = P.builtin_model("inception_chain", 32)
+    dev = P.DeviceGraph.uniform(16)
+    prep = P.PreparedPlan(g, devices=dev, ctx=gpu.ctx)
+    want = O.Instance.builtin("inception_chain", 32, "port").build_tables(16).plan()
+    for upload in (True, False, False):
+        prep.launch(upload)
+        r = prep.fetch()
+        assert list(r.indices) == list(want.indices) and r.cost == want.cost
+    prof = prep.profile()
+    kinds = [k for k, _, _ in prof]
+    assert kinds[0] == "tables" and kinds.count("wave") == r.waves and kinds[-3:] == ["enumerate", "finish", "d2h"]
+    assert sum(w for k, _, w in prof if k == "wave") > 0
+
+
+def test_library_generators_match_reference_draw_order(gpu):
+    import paper_1802_04924_b200 as P
+
+    for seed in range(40):
+        n, mc, bp = 1 + seed % 9, 1 + seed % 4, 0.35 * (seed % 3)
+        g, t = P.random_series_parallel_graph(seed, n, mc, bp, 4, ctx=gpu.ctx)
+        ref = O.Instance.random(seed, n, mc, bp, 4, "port")
+        cat, node, _, _, xfer = t.download()
+        assert all((bits(a) == bits(b)).all() for a, b in zip(node, ref.nodes()))
+        assert all((bits(a) == bits(b)).all() for a, b in zip(xfer, ref.xfers()))
+        r = P.plan_with_tables(g, t)
+        assert r.cost == ref.plan().cost
+    g = P.series_parallel_graph(1, 1000, 0.3)
+    ref = O.Instance.synthetic(1, 1000, 2, 0.3, "port")
+    assert g.n_layers == ref.n_layers and (np.stack(g.edges()) == np.stack(ref.edges())).all()
+
+
+def test_device_synthetic_tables(gpu):
+    import paper_1802_04924_b200 as P
+
+    g = P.series_parallel_graph(5, 200, 0.3)
+    t = P.synthetic_cost_tables(g, 48, seed=9, ctx=gpu.ctx)
+    cat, node, _, _, xfer = t.download()
+    assert all(((v * 64) == np.floor(v * 64)).all() and v.min() >= 0 and v.max() <= 10 for v in node + xfer)
+    # the same tables through the host upload path and the FP64 path agree
+    inst_nodes, inst_xfer = node, xfer
+    ctx64 = P.Context(0, precision="fp64")
+    t64 = P.upload_cost_tables(g, cat, inst_nodes, inst_xfer, ctx64)
+    a, b = P.plan_with_tables(g, t), P.plan_with_tables(g, t64)
+    assert a.precision == "fixed" and b.precision == "fp64"
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
