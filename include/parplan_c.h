@@ -144,6 +144,9 @@ pp_status pp_context_create_on_stream(int32_t device, void *cuda_stream, pp_cont
 pp_status pp_context_stream(const pp_context *ctx, void **cuda_stream);
 pp_status pp_context_destroy(pp_context *ctx);
 pp_status pp_context_set_precision(pp_context *ctx, int32_t policy);
+/* 0 (default): large certified fixed-point folds use the S16x2 min-plus
+ * kernel; 1: every fold uses the generic tiled kernel (for parity checks). */
+pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy);
 /* kernel launches issued on this context since creation */
 pp_status pp_context_launch_count(const pp_context *ctx, int64_t *launches);
 

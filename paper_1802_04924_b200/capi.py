@@ -85,6 +85,7 @@ _SIGS = {
     "pp_plan_profile": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, C.POINTER(C.c_int32)]),
     "pp_context_destroy": (C.c_int, [_vp]),
     "pp_context_set_precision": (C.c_int, [_vp, C.c_int32]),
+    "pp_context_set_kernel_policy": (C.c_int, [_vp, C.c_int32]),
     "pp_context_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "pp_graph_create": (C.c_int, [C.POINTER(_GraphDesc), _pp]),
     "pp_graph_builtin": (C.c_int, [C.c_char_p, C.c_int64, _pp]),
@@ -191,6 +192,10 @@ class Context:
 
     def set_precision(self, precision: str) -> None:
         _check(lib().pp_context_set_precision(self.h, {"auto": 0, "fp64": 1}[precision]))
+
+    def set_kernel_policy(self, policy: str) -> None:
+        """'auto' (S16x2 min-plus for large certified folds) or 'generic' (tiled fold only)."""
+        _check(lib().pp_context_set_kernel_policy(self.h, {"auto": 0, "generic": 1}[policy]))
 
     @property
     def launches(self) -> int:
@@ -554,7 +559,8 @@ class PreparedPlan:
         _check(lib().pp_plan_profile(self.h, 0, None, None, None, C.byref(n)))
         ms, kind, work = np.zeros(n.value), np.zeros(n.value, np.int32), np.zeros(n.value)
         _check(lib().pp_plan_profile(self.h, n.value, _ptr(ms), _ptr(kind), _ptr(work), C.byref(n)))
-        names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h"}
+        names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h", 5: "memset", 6: "mp_reduce",
+                 7: "mp_pack", 8: "mp_fold", 9: "mp_rescan"}
         return [(names[int(k)], float(m), float(w)) for k, m, w in zip(kind, ms, work)]
 
     def __del__(self):

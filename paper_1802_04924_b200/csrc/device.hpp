@@ -103,6 +103,7 @@ struct pp_context {
   bool external_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int precision = PP_PRECISION_AUTO;
+  bool no_minplus = false; // kernel policy: generic tiled fold only (parity tests)
   int64_t launches = 0;
   pp::DBuf<unsigned char> desc;  // device image of the current call's descriptors
   pp::PinnedBuf staging;         // pinned host side of desc + results

@@ -11,6 +11,7 @@
 // fetch:                 stream sync, parse results
 #include "dp.hpp"
 #include "kernels.cuh"
+#include "minplus.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -141,10 +142,87 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           if (in >= t.ne) tab_plan.release(tab_off[static_cast<size_t>(in)], cells(in) * sizeof(T));
       }
   }
+  // ---- large fixed-point folds: span certificate + per-wave scratch -----------
+  // Span bounds per table (rows: max over rows of max-min; cols likewise),
+  // propagated through the log: fold R(out) <= R(t2), K(out) <= K(t1);
+  // merge R = R1 + R2, K = K1 + K2.  A fold takes the S16x2 kernel when
+  // rowspan(w + t1) <= 16383 and colspan(t2) <= 16382 (minplus.cuh).
+  std::vector<char> large(s.ops.size(), 0);
+  struct MpLayout {
+    size_t ra, cb, A2T, A16, B16, B16T, P;
+    int nup, nwp, nvp, splits, cps;
+  };
+  std::vector<MpLayout> mpl(s.ops.size());
+  size_t mp_bytes = 0;
+  if constexpr (std::is_same_v<T, int32_t>) {
+    std::vector<int64_t> R(static_cast<size_t>(E_total), 0), Kc(static_cast<size_t>(E_total), 0);
+    for (int e = 0; e < t.ne; ++e) {
+      R[static_cast<size_t>(e)] = t.row_span[static_cast<size_t>(e)];
+      Kc[static_cast<size_t>(e)] = t.col_span[static_cast<size_t>(e)];
+    }
+    for (size_t oi = 0; oi < s.ops.size(); ++oi) {
+      const Op &op = s.ops[oi];
+      const size_t a = static_cast<size_t>(op.e1), b2 = static_cast<size_t>(op.e2), o = static_cast<size_t>(op.ne);
+      if (op.type) {
+        R[o] = R[a] + R[b2];
+        Kc[o] = Kc[a] + Kc[b2];
+        continue;
+      }
+      R[o] = R[b2];
+      Kc[o] = Kc[a];
+      const int nu = rows[a], nw = t.counts[static_cast<size_t>(op.removed)], nv = cols[b2];
+      const int64_t spanA = t.node_span[static_cast<size_t>(op.removed)] + R[a], spanB = Kc[b2];
+      large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && spanA <= kMpPad && spanB <= kMpPad - 1 && !ctx->no_minplus;
+    }
+    for (int w = 1; w <= s.n_waves; ++w) {
+      int64_t tiles = 0;
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        if (!large[static_cast<size_t>(oi)]) continue;
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        tiles += static_cast<int64_t>((rows[static_cast<size_t>(op.e1)] + kMpTile - 1) / kMpTile) *
+                 ((cols[static_cast<size_t>(op.e2)] + kMpTile - 1) / kMpTile);
+      }
+      const int64_t want = std::max<int64_t>(1, (2 * int64_t(ctx->sms) + tiles - 1) / std::max<int64_t>(1, tiles));
+      size_t off = 0;
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        if (!large[static_cast<size_t>(oi)]) continue;
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        MpLayout &L = mpl[static_cast<size_t>(oi)];
+        const int nu = rows[static_cast<size_t>(op.e1)], nw = t.counts[static_cast<size_t>(op.removed)],
+                  nv = cols[static_cast<size_t>(op.e2)];
+        L.nup = (nu + kMpTile - 1) / kMpTile * kMpTile;
+        L.nvp = (nv + kMpTile - 1) / kMpTile * kMpTile;
+        L.nwp = (nw + kMpChunk - 1) / kMpChunk * kMpChunk;
+        const int nchunks = L.nwp / kMpChunk;
+        L.splits = static_cast<int>(std::min<int64_t>(want, nchunks));
+        L.cps = (nchunks + L.splits - 1) / L.splits;
+        L.splits = (nchunks + L.cps - 1) / L.cps;
+        auto take = [&](size_t bytes) {
+          const size_t o = off;
+          off += align256(bytes);
+          return o;
+        };
+        L.ra = take(static_cast<size_t>(nu) * 4);
+        L.cb = take(static_cast<size_t>(nv) * 4);
+        L.A2T = take(static_cast<size_t>(L.nwp) * L.nup * 4);
+        L.A16 = take(static_cast<size_t>(nu) * L.nwp * 2);
+        L.B16 = take(static_cast<size_t>(L.nwp) * L.nvp * 2);
+        L.B16T = take(static_cast<size_t>(nv) * L.nwp * 2);
+        L.P = take(static_cast<size_t>(L.nup) * L.nvp * 4);
+      }
+      mp_bytes = std::max(mp_bytes, off);
+    }
+    if (mp_bytes)
+      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kMpSmem)));
+  }
+
   const size_t tables_bytes =
       bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
   const size_t off_tables = 0, off_derived = tables_bytes, off_am = off_derived + align256(tab_plan.end()),
-               off_image = off_am + align256(am_bytes);
+               off_mp = off_am + align256(am_bytes), off_image = off_mp + align256(mp_bytes);
 
   // ---- enumeration / unwind descriptors (pointer-free parts) ----------------
   std::vector<int> pos(static_cast<size_t>(t.nl), -1);
@@ -169,11 +247,16 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     int nf, nm;
     int64_t ftiles, mblocks;
     double cells;
+    size_t p0; // large folds: [p0, p0 + np) in mpf
+    int np;
+    int64_t fold_blocks, red_blocks, pack_blocks, rescan_blocks;
+    double mp_cells;
+    std::vector<std::pair<int32_t *, size_t>> p_init; // split folds: P <- 0x7f7f7f7f
   };
   struct Image {
     Packer pk;
     std::vector<WaveRange> waves;
-    size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw;
+    size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
     size_t res_bytes;
   };
   auto make_image = [&](unsigned char *db) {
@@ -192,12 +275,53 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
                                            : reinterpret_cast<const T *>(t.node32.p));
     std::vector<FoldDesc<T>> folds;
     std::vector<MergeDesc<T>> merges;
+    std::vector<MpFold> mpf;
     for (int w = 1; w <= s.n_waves; ++w) {
-      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0};
+      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, 0, 0, 0.0, {}};
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
         T *out = const_cast<T *>(tabp(op.ne));
+        if constexpr (std::is_same_v<T, int32_t>) {
+          if (large[static_cast<size_t>(oi)]) {
+            const MpLayout &L = mpl[static_cast<size_t>(oi)];
+            unsigned char *sb = db + off_mp;
+            MpFold f{};
+            f.t1 = tabp(op.e1);
+            f.t2 = tabp(op.e2);
+            f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
+            f.out = out;
+            f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
+            f.ra = reinterpret_cast<int32_t *>(sb + L.ra);
+            f.cb = reinterpret_cast<int32_t *>(sb + L.cb);
+            f.A2T = reinterpret_cast<uint32_t *>(sb + L.A2T);
+            f.A16 = reinterpret_cast<uint16_t *>(sb + L.A16);
+            f.B16 = reinterpret_cast<uint16_t *>(sb + L.B16);
+            f.B16T = reinterpret_cast<uint16_t *>(sb + L.B16T);
+            f.P = reinterpret_cast<int32_t *>(sb + L.P);
+            f.nu = rows[static_cast<size_t>(op.e1)];
+            f.nw = t.counts[static_cast<size_t>(op.removed)];
+            f.nv = cols[static_cast<size_t>(op.e2)];
+            f.nup = L.nup, f.nwp = L.nwp, f.nvp = L.nvp;
+            f.tiles_i = L.nup / kMpTile;
+            f.tiles_k = L.nvp / kMpTile;
+            f.splits = L.splits;
+            f.chunks_per_split = L.cps;
+            f.fold_begin = wr.fold_blocks;
+            wr.fold_blocks += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.splits;
+            f.red_begin = wr.red_blocks;
+            wr.red_blocks += (f.nu + kMpRedRowsPerBlock - 1) / kMpRedRowsPerBlock + (f.nv + 31) / 32;
+            f.pack_begin = wr.pack_blocks;
+            wr.pack_blocks += static_cast<int64_t>(f.nup / 32) * (f.nwp / 32) + static_cast<int64_t>(f.nwp / 32) * (f.nvp / 32);
+            f.rescan_begin = wr.rescan_blocks;
+            wr.rescan_blocks += (static_cast<int64_t>(f.nu) * f.nv + 255) / 256;
+            if (f.splits > 1) wr.p_init.push_back({f.P, static_cast<size_t>(L.nup) * L.nvp * 4});
+            wr.mp_cells += static_cast<double>(f.nu) * f.nw * f.nv;
+            mpf.push_back(f);
+            ++wr.np;
+            continue;
+          }
+        }
         if (!op.type) {
           FoldDesc<T> f;
           f.t1 = tabp(op.e1);
@@ -246,6 +370,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
                                cols[static_cast<size_t>(op.ne)]});
     }
     Packer &pk = im.pk;
+    im.oMP = pk.put(mpf);
     im.oF = pk.put(folds);
     im.oM = pk.put(merges);
     im.oN = pk.put(en);
@@ -330,6 +455,44 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ++launches;
   }
   for (const auto &wr : im.waves) {
+    if (wr.np > 0) { // large fixed-point folds of this wave: reduce -> pack -> fold -> rescan
+      const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + wr.p0;
+      const int np = wr.np;
+      for (const auto &pi : wr.p_init) {
+        int32_t *pp = pi.first;
+        const size_t nb = pi.second;
+        P->steps.push_back([pp, nb](cudaStream_t st) { PP_CUDA(cudaMemsetAsync(pp, 0x7f, nb, st)); });
+        P->step_kind.push_back(5);
+        P->step_work.push_back(static_cast<double>(nb));
+      }
+      const int64_t rb = wr.red_blocks, pb = wr.pack_blocks, fb = wr.fold_blocks, sb = wr.rescan_blocks;
+      PP_REQUIRE(fb < (int64_t(1) << 31) && pb < (int64_t(1) << 31) && sb < (int64_t(1) << 31), "wave too large");
+      P->steps.push_back([ctx, mf, np, rb](cudaStream_t st) {
+        mp_reduce_kernel<<<static_cast<unsigned>(rb), 256, 0, st>>>(mf, np);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(6);
+      P->step_work.push_back(0.0);
+      P->steps.push_back([ctx, mf, np, pb](cudaStream_t st) {
+        mp_pack_kernel<<<static_cast<unsigned>(pb), 256, 0, st>>>(mf, np);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(7);
+      P->step_work.push_back(0.0);
+      P->steps.push_back([ctx, mf, np, fb](cudaStream_t st) {
+        mp_fold_kernel<<<static_cast<unsigned>(fb), kMpThreads, kMpSmem, st>>>(mf, np);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(8);
+      P->step_work.push_back(wr.mp_cells);
+      P->steps.push_back([ctx, mf, np, sb](cudaStream_t st) {
+        mp_rescan_kernel<<<static_cast<unsigned>(sb), 256, 0, st>>>(mf, np);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(9);
+      P->step_work.push_back(0.0);
+      launches += 4;
+    }
     const int64_t grid = wr.ftiles + wr.mblocks;
     if (!grid) continue;
     PP_REQUIRE(grid < (int64_t(1) << 31), "wave too large for one launch");

@@ -132,6 +132,14 @@ pp_status pp_context_set_precision(pp_context *ctx, int32_t policy) {
   });
 }
 
+pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy) {
+  return guard([&] {
+    PP_REQUIRE(ctx, "null context");
+    PP_REQUIRE(policy == 0 || policy == 1, "unknown kernel policy");
+    ctx->no_minplus = policy == 1;
+  });
+}
+
 pp_status pp_context_launch_count(const pp_context *ctx, int64_t *n) {
   return guard([&] {
     PP_REQUIRE(ctx && n, "null argument");

@@ -1,0 +1,72 @@
+"""The S16x2 min-plus fold (minplus.cuh) against the generic tiled fold and
+the CPU oracle: values, argmins (lowest-index ties), padding at sizes that are
+not multiples of the 128x128 tile / 32-j chunk, split-j CTAs, tie-heavy data."""
+import numpy as np
+import pytest
+
+import oracle as O
+from impls import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _chain(P, n):
+    layers = [P.Layer("u", "input", [4, 1, 1])] + [P.Layer(f"n{i}", "softmax") for i in range(1, n)]
+    inputs = [[]] + [[layers[i - 1].id] for i in range(1, n)]
+    return P.ComputationGraph.create(layers, inputs, 8)
+
+
+def _tables(rng, counts, edges, hi):
+    node = [rng.integers(0, hi, c) / 64.0 for c in counts]
+    xfer = [rng.integers(0, hi, (counts[s], counts[d])) / 64.0 for s, d in edges]
+    return node, xfer
+
+
+@pytest.mark.parametrize("sizes,hi", [((300, 200, 257), 641), ((129, 70, 1000), 3), ((64, 64, 64), 2),
+                                      ((1024, 96, 512), 641), ((130, 2048, 66), 5)])
+def test_fold_matches_generic_and_oracle(gpu, sizes, hi):
+    import paper_1802_04924_b200 as P
+
+    rng = np.random.default_rng(sum(sizes) + hi)
+    nu, nw, nv = sizes
+    g = _chain(P, 3)
+    counts = [nu, nw, nv]
+    node, xfer = _tables(rng, counts, [(0, 1), (1, 2)], hi)
+    cat = [np.tile([1, 1, 1, 1], (c, 1)) for c in counts]
+    fast = P.Context(0)
+    slow = P.Context(0)
+    slow.set_kernel_policy("generic")
+    ra = P.ReducedGraph(g, P.upload_cost_tables(g, cat, node, xfer, fast))
+    tf = P.upload_cost_tables(g, cat, node, xfer, fast)
+    ts = P.upload_cost_tables(g, cat, node, xfer, slow)
+    pf = P.PreparedPlan(g, tables=tf, ctx=fast)
+    kinds = [k for k, _, _ in pf.profile()]
+    assert "mp_fold" in kinds, kinds
+    a = P.plan_with_tables(g, tf)
+    b = P.plan_with_tables(g, ts)
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
+    # the fold's table and argmin (step API uses the generic kernel) vs the oracle
+    want_t, want_am = O.fold(node[1], xfer[0], xfer[1])
+    ra.node_elimination()
+    assert (bits(ra.edge_table(2)) == bits(want_t)).all()
+    assert (ra.argmin(0) == want_am).all()
+    # the plan's unwound middle index equals the oracle argmin at the chosen endpoints
+    assert a.indices[1] == want_am[a.indices[0], a.indices[2]]
+
+
+@pytest.mark.parametrize("C", [96, 200, 512])
+def test_synthetic_graph_fast_vs_generic(gpu, C):
+    import paper_1802_04924_b200 as P
+
+    g = P.series_parallel_graph(11, 120, 0.4)
+    fast = P.Context(0)
+    slow = P.Context(0)
+    slow.set_kernel_policy("generic")
+    tf = P.synthetic_cost_tables(g, C, seed=3, ctx=fast)
+    cat, node, _, _, xfer = tf.download()
+    ts = P.upload_cost_tables(g, cat, node, xfer, slow)
+    a = P.plan_with_tables(g, tf)
+    b = P.plan_with_tables(g, ts)
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
+    prof = P.PreparedPlan(g, tables=tf, ctx=fast).profile()
+    assert sum(w for k, _, w in prof if k == "mp_fold") > 0

@@ -22,8 +22,11 @@ __device__ __forceinline__ float min3f(float a, float b, float c) {
   return d;
 }
 
+__device__ unsigned long long g_clk[2];
+
 template <int V>
 __global__ void __launch_bounds__(256, 1) bench(const float *gA, const float *gB, float *out, int R) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_clk[0] = clock64();
   __shared__ __align__(16) float As[BK][TILE];
   __shared__ __align__(16) float Bs[BK][TILE];
   for (int t = threadIdx.x; t < BK * TILE; t += 256) {
@@ -141,6 +144,47 @@ __global__ void __launch_bounds__(256, 1) bench(const float *gA, const float *gB
     for (int r = 0; r < 8; ++r)
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc += (float)(best[r][c] + idx[r][c]);
+  } else if constexpr (V == 7 || V == 8) {
+    // 16-bit pairs: a duplicated in both halves (int32 words), b = two adjacent columns per word
+    const unsigned *Au = reinterpret_cast<const unsigned *>(&As[0][0]);
+    const unsigned *Bu = reinterpret_cast<const unsigned *>(&Bs[0][0]);
+    unsigned best[8][4], m[8][4], idx[8][4];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) best[r][c] = 0x7fff7fffu, idx[r][c] = 0;
+    for (int it = 0; it < R; ++it) {
+      asm volatile("" ::: "memory");
+      const unsigned cid = (unsigned)it * 0x10001u;
+#pragma unroll 4
+      for (int j = 0; j < BK; ++j) {
+        unsigned a[8], b[4];
+        *(uint4 *)&a[0] = *(const uint4 *)&Au[j * TILE + ty * 8];
+        *(uint4 *)&a[4] = *(const uint4 *)&Au[j * TILE + ty * 8 + 4];
+        *(uint4 *)&b[0] = *(const uint4 *)&Bu[j * TILE + tx * 4];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if constexpr (V == 7) best[r][c] = __viaddmin_s16x2(a[r], b[c], best[r][c]);
+            else m[r][c] = (j == 0) ? __vadd2(a[r], b[c]) : __viaddmin_s16x2(a[r], b[c], m[r][c]);
+          }
+      }
+      if constexpr (V == 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const unsigned lt = __vcmplts2(m[r][c], best[r][c]);
+            best[r][c] = __vmins2(best[r][c], m[r][c]);
+            idx[r][c] = (idx[r][c] & ~lt) | (cid & lt);
+          }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc += (float)(best[r][c] ^ idx[r][c]);
   } else if constexpr (V == 4) {
     double best[4][8];
 #pragma unroll
@@ -168,6 +212,7 @@ __global__ void __launch_bounds__(256, 1) bench(const float *gA, const float *gB
       for (int c = 0; c < 8; ++c) acc += (float)best[r][c];
   }
   out[blockIdx.x * 256 + threadIdx.x] = acc;
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_clk[1] = clock64();
 }
 
 template <int V>
@@ -188,8 +233,13 @@ double run(const char *name, const float *dA, const float *dB, float *dO, int sm
   cudaEventElapsedTime(&ms, e0, e1);
   double cells = (double)grid * 256 * cells_per_thread_per_j * BK * R;
   double rate = cells / (ms * 1e-3);
-  printf("{\"variant\": \"%s\", \"occ\": %d, \"ms\": %.3f, \"cells_per_s\": %.4e, \"cells_per_clk_per_sm\": %.2f, \"err\": \"%s\"}\n", name, occ, ms, rate,
-         rate / sms / 1.965e9, cudaGetErrorString(cudaGetLastError()));
+  unsigned long long clk[2];
+  cudaMemcpyFromSymbol(clk, g_clk, sizeof clk);
+  const double cyc = (double)(clk[1] - clk[0]);  // block 0's span ~ whole kernel (one wave)
+  const double mhz = cyc / (ms * 1e3);
+  printf("{\"variant\": \"%s\", \"occ\": %d, \"ms\": %.3f, \"cells_per_s\": %.4e, \"sm_mhz_est\": %.0f, "
+         "\"cells_per_clk_per_sm\": %.2f, \"err\": \"%s\"}\n",
+         name, occ, ms, rate, mhz, cells / cyc / sms, cudaGetErrorString(cudaGetLastError()));
   return rate;
 }
 
@@ -215,5 +265,7 @@ int main(int argc, char **argv) {
   run<6>("s32 VIADDMNMX + chunk argmin", dA, dB, dO, sms, R, 64);
   run<3>("ffma (peak ref)", dA, dB, dO, sms, R, 64);
   run<4>("f64 DADD+DMNMX", dA, dB, dO, sms, R / 4, 32);
+  run<7>("s16x2 VIADDMNMX.S16x2", dA, dB, dO, sms, R, 64);
+  run<8>("s16x2 + chunk argmin", dA, dB, dO, sms, R, 64);
   return 0;
 }
