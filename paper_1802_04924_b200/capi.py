@@ -194,8 +194,11 @@ class Context:
         _check(lib().pp_context_set_precision(self.h, {"auto": 0, "fp64": 1}[precision]))
 
     def set_kernel_policy(self, policy: str) -> None:
-        """'auto' (S16x2 min-plus for large certified folds) or 'generic' (tiled fold only)."""
-        _check(lib().pp_context_set_kernel_policy(self.h, {"auto": 0, "generic": 1}[policy]))
+        """'auto': S16x2 min-plus for large certified folds, one fused cooperative kernel
+        for plans without them; 'generic': tiled fold only; 'unfused': one launch per
+        wave; 'generic_unfused': both."""
+        _check(lib().pp_context_set_kernel_policy(
+            self.h, {"auto": 0, "generic": 1, "unfused": 2, "generic_unfused": 3}[policy]))
 
     @property
     def launches(self) -> int:
@@ -560,7 +563,8 @@ class PreparedPlan:
         ms, kind, work = np.zeros(n.value), np.zeros(n.value, np.int32), np.zeros(n.value)
         _check(lib().pp_plan_profile(self.h, n.value, _ptr(ms), _ptr(kind), _ptr(work), C.byref(n)))
         names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h", 5: "memset", 6: "mp_reduce",
-                 7: "mp_pack", 8: "mp_fold", 9: "mp_rescan"}
+                 7: "mp_pack", 8: "mp_fold", 9: "mp_rescan", 10: "fused", 11: "fused.tables",
+                 12: "fused.wave", 13: "fused.enumerate", 14: "fused.finish"}
         return [(names[int(k)], float(m), float(w)) for k, m, w in zip(kind, ms, work)]
 
     def __del__(self):

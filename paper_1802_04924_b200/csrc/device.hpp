@@ -103,7 +103,8 @@ struct pp_context {
   bool external_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int precision = PP_PRECISION_AUTO;
-  bool no_minplus = false; // kernel policy: generic tiled fold only (parity tests)
+  bool no_minplus = false; // kernel policy bit 0: generic tiled fold only (parity tests)
+  bool no_fused = false;   // kernel policy bit 1: one launch per wave instead of the fused kernel
   int64_t launches = 0;
   pp::DBuf<unsigned char> desc;  // device image of the current call's descriptors
   pp::PinnedBuf staging;         // pinned host side of desc + results

@@ -47,7 +47,7 @@ static void enumerate_impl(pp_context *ctx, const std::vector<EnumNode> &en, con
   fa.final_cost = reinterpret_cast<double *>(b + oFC);
   fa.shift = shift;
   fa.n_rec = -1;
-  finish_kernel<T><<<1, 32, 0, ctx->stream>>>(fa);
+  finish_kernel<T><<<1, kFinishThreads, 0, ctx->stream>>>(fa);
   check_launch(ctx);
   unsigned char *h = static_cast<unsigned char *>(ctx->staging.p);
   PP_CUDA(cudaMemcpyAsync(h + oOut, b + oOut, oFC + 8 - oOut, cudaMemcpyDeviceToHost, ctx->stream));

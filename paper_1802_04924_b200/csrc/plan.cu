@@ -10,6 +10,7 @@
 //                        for prepared plans
 // fetch:                 stream sync, parse results
 #include "dp.hpp"
+#include "fused.cuh"
 #include "kernels.cuh"
 #include "minplus.cuh"
 
@@ -82,6 +83,9 @@ struct pp_prepared {
   std::vector<int32_t> step_kind; // 0 K1/K2, 1 wave, 2 K5, 3 finish, 4 D2H
   std::vector<double> step_work;  // cells: K1/K2 table cells, wave min-plus cells (nu*nw*nv) + merge cells
   bool launched = false, uploaded = false;
+  size_t stamp_off = 0; // fused kernel phase stamps (image offset), n_stamps entries
+  int n_stamps = 0;
+  std::vector<double> fused_wave_work;
 
   ~pp_prepared() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -257,6 +261,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     Packer pk;
     std::vector<WaveRange> waves;
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
+    size_t oG, oT, oFW, oST;
+    int nG;
     size_t res_bytes;
   };
   auto make_image = [&](unsigned char *db) {
@@ -362,17 +368,35 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     for (int id : s.final_edges)
       ee.push_back(EnumEdge{tabp(id), pos[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])],
                             pos[static_cast<size_t>(s.edst[static_cast<size_t>(id)])], cols[static_cast<size_t>(id)], 0});
+    // unwind records grouped by wave, last wave first (kernels.cuh finish_kernel)
     std::vector<UnwindRec> recs;
-    for (size_t oi = 0; oi < s.ops.size(); ++oi) {
-      const Op &op = s.ops[oi];
-      if (op.type) continue;
-      recs.push_back(UnwindRec{reinterpret_cast<const uint16_t *>(db + off_am + am_off[oi]), op.removed, op.u, op.v,
-                               cols[static_cast<size_t>(op.ne)]});
+    std::vector<int32_t> groups{0};
+    for (int w = s.n_waves; w >= 1; --w) {
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        if (op.type) continue;
+        recs.push_back(UnwindRec{reinterpret_cast<const uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]),
+                                 op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)]});
+      }
+      if (static_cast<int32_t>(recs.size()) > groups.back()) groups.push_back(static_cast<int32_t>(recs.size()));
     }
     Packer &pk = im.pk;
+    im.oG = pk.put(groups);
+    im.nG = static_cast<int>(groups.size()) - 1;
+    im.oT = pk.put(std::vector<double>(static_cast<size_t>(t.nl + t.ne)));
     im.oMP = pk.put(mpf);
     im.oF = pk.put(folds);
     im.oM = pk.put(merges);
+    { // per-wave work lists of the fused kernel (pointers into the sections above)
+      std::vector<FusedWave<T>> fw;
+      for (const auto &wr : im.waves)
+        fw.push_back(FusedWave<T>{reinterpret_cast<const FoldDesc<T> *>(db + off_image + im.oF) + wr.f0,
+                                  reinterpret_cast<const MergeDesc<T> *>(db + off_image + im.oM) + wr.m0, wr.nf, wr.nm,
+                                  wr.ftiles, wr.ftiles + wr.mblocks});
+      im.oFW = pk.put(fw);
+      im.oST = pk.put(std::vector<uint64_t>(im.waves.size() + 4));
+    }
     im.oN = pk.put(en);
     im.oE = pk.put(ee);
     im.oR = pk.put(recs);
@@ -436,18 +460,23 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->step_kind.clear();
   P->step_work.clear();
   int launches = 0;
-  if (bp && bp->grid > 0) {
-    BuildArgs a;
-    a.layers = reinterpret_cast<const LayerDev *>(dimg + im.oLay);
-    a.edges = reinterpret_cast<const EdgeDev *>(dimg + im.oEdg);
-    a.cfg = reinterpret_cast<const int64_t *>(dimg + im.oCfg);
-    a.rates = reinterpret_cast<const double *>(dimg + im.oRat);
-    a.bw = reinterpret_cast<const double *>(dimg + im.oBw);
-    a.node = t.node.p, a.compute = t.compute.p, a.sync = t.sync.p, a.xfer = t.xfer64.p;
-    a.ncells = t.ncells;
-    a.nl = t.nl, a.ne = t.ne, a.D = bp->D;
-    a.node_blocks = static_cast<int32_t>(bp->node_blocks);
-    a.bw_uniform = bp->bw_uniform;
+  // one cooperative kernel for the whole plan when no fold needs the S16x2 path
+  const bool use_fused = mp_bytes == 0 && !ctx->no_fused;
+  BuildArgs ba{};
+  if (bp) {
+    ba.layers = reinterpret_cast<const LayerDev *>(dimg + im.oLay);
+    ba.edges = reinterpret_cast<const EdgeDev *>(dimg + im.oEdg);
+    ba.cfg = reinterpret_cast<const int64_t *>(dimg + im.oCfg);
+    ba.rates = reinterpret_cast<const double *>(dimg + im.oRat);
+    ba.bw = reinterpret_cast<const double *>(dimg + im.oBw);
+    ba.node = t.node.p, ba.compute = t.compute.p, ba.sync = t.sync.p, ba.xfer = t.xfer64.p;
+    ba.ncells = t.ncells;
+    ba.nl = t.nl, ba.ne = t.ne, ba.D = bp->D;
+    ba.node_blocks = static_cast<int32_t>(bp->node_blocks);
+    ba.bw_uniform = bp->bw_uniform;
+  }
+  if (bp && bp->grid > 0 && !use_fused) {
+    const BuildArgs a = ba;
     const int64_t grid = bp->grid;
     P->steps.push_back([ctx, a, grid](cudaStream_t st) { launch_build(ctx, st, a, grid); });
     P->step_kind.push_back(0);
@@ -455,6 +484,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ++launches;
   }
   for (const auto &wr : im.waves) {
+    if (use_fused) break;
     if (wr.np > 0) { // large fixed-point folds of this wave: reduce -> pack -> fold -> rescan
       const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + wr.p0;
       const int np = wr.np;
@@ -514,12 +544,14 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     const int m = static_cast<int>(s.final_edges.size());
     A *bv = reinterpret_cast<A *>(dimg + im.oBV);
     int64_t *bi = reinterpret_cast<int64_t *>(dimg + im.oBI);
-    P->steps.push_back([ctx, en, K, ee, m, space, per_thread, bv, bi, nblk](cudaStream_t st) {
-      enum_kernel<T><<<nblk, kEnumThreads, 0, st>>>(en, K, ee, m, space, per_thread, bv, bi);
-      check_launch(ctx);
-    });
-    P->step_kind.push_back(2);
-    P->step_work.push_back(static_cast<double>(space));
+    if (!use_fused) {
+      P->steps.push_back([ctx, en, K, ee, m, space, per_thread, bv, bi, nblk](cudaStream_t st) {
+        enum_kernel<T><<<nblk, kEnumThreads, 0, st>>>(en, K, ee, m, space, per_thread, bv, bi);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(2);
+      P->step_work.push_back(static_cast<double>(space));
+    }
     FinishArgs fa{};
     fa.blk_val = bv;
     fa.blk_idx = bi;
@@ -534,6 +566,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.shift = t.shift;
     fa.recs = reinterpret_cast<const UnwindRec *>(dimg + im.oR);
     fa.n_rec = static_cast<int>(s.node_ops);
+    fa.group_begin = reinterpret_cast<const int32_t *>(dimg + im.oG);
+    fa.n_groups = im.nG;
+    fa.terms = reinterpret_cast<double *>(dimg + im.oT);
     fa.nl = t.nl;
     fa.onode = bp ? static_cast<const void *>(t.node.p)
                   : (t.mode == kFP64 ? static_cast<const void *>(t.node.p) : static_cast<const void *>(t.node32.p));
@@ -545,13 +580,54 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.edst = reinterpret_cast<const int32_t *>(dimg + im.oD);
     fa.counts = reinterpret_cast<const int32_t *>(dimg + im.oC);
     fa.ne = t.ne;
-    P->steps.push_back([ctx, fa](cudaStream_t st) {
-      finish_kernel<T><<<1, 32, 0, st>>>(fa);
-      check_launch(ctx);
-    });
-    P->step_kind.push_back(3);
-    P->step_work.push_back(0.0);
-    launches += 2;
+    if (!use_fused) {
+      P->steps.push_back([ctx, fa](cudaStream_t st) {
+        finish_kernel<T><<<1, kFinishThreads, 0, st>>>(fa);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(3);
+      P->step_work.push_back(0.0);
+      launches += 2;
+    } else {
+      FusedArgs<T> fz{};
+      fz.has_build = bp != nullptr;
+      fz.build = ba;
+      fz.xcells = bp ? t.xcells : 0;
+      fz.waves = reinterpret_cast<const FusedWave<T> *>(dimg + im.oFW);
+      fz.n_waves = static_cast<int32_t>(im.waves.size());
+      fz.en = en, fz.ee = ee, fz.k = K, fz.m = m;
+      fz.space = space, fz.per_thread = per_thread;
+      fz.blk_val = bv, fz.blk_idx = bi, fz.nblk = nblk;
+      fz.fin = fa;
+      fz.stamps = reinterpret_cast<uint64_t *>(dimg + im.oST);
+      P->stamp_off = im.oST;
+      P->n_stamps = static_cast<int>(im.waves.size()) + 4; // start, tables, waves..., enum, finish
+      P->fused_wave_work.clear();
+      for (const auto &wr : im.waves) P->fused_wave_work.push_back(wr.cells);
+      int occ = 0;
+      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_fused_kernel<T>, kFusedThreads, 0));
+      PP_REQUIRE(occ > 0, "fused plan kernel does not fit on an SM");
+      int64_t items = std::max<int64_t>(nblk, 1);
+      if (bp) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
+      for (const auto &wr : im.waves) items = std::max<int64_t>(items, wr.ftiles + wr.mblocks);
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, int64_t(ctx->sms) * occ));
+      P->steps.push_back([ctx, fz, grid](cudaStream_t st) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kFusedThreads);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PP_CUDA(cudaLaunchKernelEx(&cfg, dp_fused_kernel<T>, fz));
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(10);
+      P->step_work.push_back(static_cast<double>(bp ? t.ncells + t.xcells : 0));
+      launches += 1;
+    }
   }
   unsigned char *hres = P->hbase + P->res_off, *dres = dimg + P->res_off;
   const size_t rb = P->res_bytes;
@@ -711,8 +787,6 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
     PP_REQUIRE(P && n_steps, "null argument");
     pp_context *ctx = P->ctx;
     const int n = static_cast<int>(P->steps.size());
-    *n_steps = n;
-    if (!step_ms || cap <= 0) return;
     std::vector<cudaEvent_t> ev(static_cast<size_t>(n) + 1);
     for (auto &e : ev) PP_CUDA(cudaEventCreate(&e));
     PP_CUDA(cudaSetDevice(ctx->device));
@@ -726,12 +800,39 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
       PP_CUDA(cudaEventRecord(ev[static_cast<size_t>(k) + 1], ctx->stream));
     }
     PP_CUDA(cudaEventSynchronize(ev.back()));
-    for (int k = 0; k < n && k < cap; ++k) {
+    std::vector<double> ms_v, work_v;
+    std::vector<int32_t> kind_v;
+    for (int k = 0; k < n; ++k) {
       float ms = 0.f;
       PP_CUDA(cudaEventElapsedTime(&ms, ev[static_cast<size_t>(k)], ev[static_cast<size_t>(k) + 1]));
-      step_ms[k] = ms;
-      if (step_kind) step_kind[k] = P->step_kind[static_cast<size_t>(k)];
-      if (step_work) step_work[k] = P->step_work[static_cast<size_t>(k)];
+      const int kind = P->step_kind[static_cast<size_t>(k)];
+      if (kind == 10 && P->n_stamps > 1) { // fused kernel: expand its phases (globaltimer stamps)
+        std::vector<uint64_t> st(static_cast<size_t>(P->n_stamps));
+        PP_CUDA(cudaMemcpy(st.data(), P->dbase + P->image_off + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
+        const int waves = P->n_stamps - 4;
+        for (int ph = 0; ph + 1 < P->n_stamps; ++ph) {
+          const int pk = ph == 0 ? 11 : ph <= waves ? 12 : ph == waves + 1 ? 13 : 14;
+          kind_v.push_back(pk);
+          ms_v.push_back(static_cast<double>(st[static_cast<size_t>(ph) + 1] - st[static_cast<size_t>(ph)]) * 1e-6);
+          work_v.push_back(pk == 11 ? P->step_work[static_cast<size_t>(k)]
+                                    : pk == 12 ? P->fused_wave_work[static_cast<size_t>(ph - 1)] : 0.0);
+        }
+        kind_v.push_back(10); // launch + residual (kernel time not covered by phases)
+        double covered = 0.0;
+        for (size_t q = ms_v.size() - static_cast<size_t>(P->n_stamps - 1); q < ms_v.size(); ++q) covered += ms_v[q];
+        ms_v.push_back(std::max(0.0, ms - covered));
+        work_v.push_back(0.0);
+        continue;
+      }
+      kind_v.push_back(kind);
+      ms_v.push_back(ms);
+      work_v.push_back(P->step_work[static_cast<size_t>(k)]);
+    }
+    *n_steps = static_cast<int32_t>(kind_v.size());
+    for (size_t k = 0; k < kind_v.size() && static_cast<int>(k) < cap && step_ms; ++k) {
+      step_ms[k] = ms_v[k];
+      if (step_kind) step_kind[k] = kind_v[k];
+      if (step_work) step_work[k] = work_v[k];
     }
     for (auto &e : ev) cudaEventDestroy(e);
   });

@@ -13,6 +13,7 @@
 // Compiled with --fmad=false: every FP64 expression keeps the reference's
 // operation order and rounding.
 #include "tables.hpp"
+#include "build.cuh"
 
 #include "parplan/geometry.hpp"
 
@@ -135,8 +136,9 @@ pp_status pp_context_set_precision(pp_context *ctx, int32_t policy) {
 pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy) {
   return guard([&] {
     PP_REQUIRE(ctx, "null context");
-    PP_REQUIRE(policy == 0 || policy == 1, "unknown kernel policy");
-    ctx->no_minplus = policy == 1;
+    PP_REQUIRE(policy >= 0 && policy <= 3, "unknown kernel policy");
+    ctx->no_minplus = (policy & 1) != 0;
+    ctx->no_fused = (policy & 2) != 0;
   });
 }
 
@@ -154,75 +156,6 @@ pp_status pp_context_launch_count(const pp_context *ctx, int64_t *n) {
 // ---------------------------------------------------------------------------
 
 namespace pp {
-
-constexpr int kBuildThreads = 128;
-
-__device__ void node_cost_cell(const BuildArgs &a, int64_t gi) {
-  // layer with cat_off <= gi < cat_off + count (binary search)
-  int lo = 0, hi = a.nl - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.layers[mid].cat_off <= gi)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  const LayerDev &L = a.layers[lo];
-  const int64_t *c = a.cfg + 4 * gi;
-  const int64_t total = c[0] * c[1] * c[2] * c[3];
-  // compute_cost (cost.hpp:60-72)
-  const int64_t flops = geo::layer_flops(L.kind, L.params, L.shape, L.in_shape);
-  double tc = 0.0;
-  if (flops != 0) {
-    double slowest = a.rates[0];
-    for (int64_t p = 1; p < total; ++p) slowest = fmin(slowest, a.rates[p]);
-    tc = geo::compute_seconds(flops, total, slowest);
-  }
-  // sync_cost (cost.hpp:79-94): sequential sum, reference order
-  const double P = geo::parameter_bytes(L.kind, L.params, L.shape, L.in_shape);
-  double ts = 0.0;
-  if (P != 0.0 && total / c[1] != 1) {
-    const double shard = P / static_cast<double>(c[1]);
-    for (int64_t p = 1; p < total; ++p) ts = ts + 2.0 * shard / a.bw[p * a.D + 0];
-  }
-  a.compute[gi] = tc;
-  a.sync[gi] = ts;
-  a.node[gi] = tc + ts;
-}
-
-__device__ void xfer_cell(const BuildArgs &a, const EdgeDev &E, int64_t cell) {
-  const int64_t i = cell / E.nv, j = cell - (cell / E.nv) * E.nv;
-  const int64_t *cs = a.cfg + 4 * (E.cat_u + i);
-  const int64_t *cd = a.cfg + 4 * (E.cat_v + j);
-  const int64_t td = cd[0] * cd[1] * cd[2] * cd[3];
-  double seconds = 0.0;
-  if (a.bw_uniform > 0.0) {
-    int64_t maxvol = 0;
-    for (int64_t q = 0; q < td; ++q) {
-      int64_t lo[4], hi[4];
-      geo::required_box(E.kind, E.params, E.sshape, E.dshape, E.band, cd, q, lo, hi);
-      if (geo::box_volume(lo, hi) == 0) continue;
-      maxvol = geo::imax(maxvol, geo::max_offdiag_volume(E.sshape, cs, lo, hi, q));
-    }
-    if (maxvol > 0) seconds = 4.0 * static_cast<double>(maxvol) / a.bw_uniform;
-  } else {
-    const int64_t ts = cs[0] * cs[1] * cs[2] * cs[3];
-    for (int64_t q = 0; q < td; ++q) {
-      int64_t lo[4], hi[4];
-      geo::required_box(E.kind, E.params, E.sshape, E.dshape, E.band, cd, q, lo, hi);
-      if (geo::box_volume(lo, hi) == 0) continue;
-      for (int64_t p = 0; p < ts; ++p) {
-        if (p == q) continue;
-        int64_t olo[4], ohi[4];
-        geo::owned_box(E.sshape, cs, p, olo, ohi);
-        int64_t vol = 1;
-        for (int d = 0; d < 4; ++d) vol *= geo::imax(0, geo::imin(ohi[d], hi[d]) - geo::imax(olo[d], lo[d]));
-        if (vol > 0) seconds = fmax(seconds, 4.0 * static_cast<double>(vol) / a.bw[p * a.D + q]);
-      }
-    }
-  }
-  a.xfer[E.out_off + cell] = seconds;
-}
 
 __global__ void __launch_bounds__(kBuildThreads) build_tables_kernel(BuildArgs a) {
   const int b = blockIdx.x;
@@ -433,6 +366,11 @@ BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev) {
   // DeviceGraph validation (graph.hpp:193-214)
   const parplan::DeviceGraph dg(std::vector<double>(dev->compute_rates, dev->compute_rates + D),
                                 std::vector<double>(dev->bandwidth, dev->bandwidth + static_cast<size_t>(D) * D));
+  for (int l = 0; l < g.nl; ++l) { // K1 runs its region arithmetic on int32 coordinates
+    const int64_t *s = &g.shape[static_cast<size_t>(l) * 4];
+    PP_REQUIRE(s[1] * s[2] * s[3] < (int64_t(1) << 31) && s[0] < (int64_t(1) << 31),
+               "layer '" + g.g.layer(l).id + "': tensor extents exceed the int32 range of the table builder");
+  }
   std::vector<int32_t> counts;
   enumerate_catalogs(g, D, &counts, &t.configs);
   init_layout(t, g, counts);

@@ -111,8 +111,8 @@ def test_prepared_plan_and_profile(gpu):
         assert list(r.indices) == list(want.indices) and r.cost == want.cost
     prof = prep.profile()
     kinds = [k for k, _, _ in prof]
-    assert kinds[0] == "tables" and kinds.count("wave") == r.waves and kinds[-3:] == ["enumerate", "finish", "d2h"]
-    assert sum(w for k, _, w in prof if k == "wave") > 0
+    assert kinds[0] == "fused.tables" and kinds.count("fused.wave") == r.waves and kinds[-2:] == ["fused", "d2h"]
+    assert sum(w for k, _, w in prof if k == "fused.wave") > 0
 
 
 def test_library_generators_match_reference_draw_order(gpu):
@@ -146,3 +146,38 @@ def test_device_synthetic_tables(gpu):
     a, b = P.plan_with_tables(g, t), P.plan_with_tables(g, t64)
     assert a.precision == "fixed" and b.precision == "fp64"
     assert list(a.indices) == list(b.indices) and a.cost == b.cost
+
+
+@pytest.mark.parametrize("model,D", [("alexnet", 4), ("vgg16", 16), ("inception_chain", 16), ("inception_chain", 64)])
+def test_fused_and_per_wave_executors_agree(gpu, model, D):
+    """One cooperative kernel for the whole plan vs one launch per wave."""
+    import paper_1802_04924_b200 as P
+
+    g = P.builtin_model(model, 32)
+    dev = P.DeviceGraph.uniform(D)
+    fused = P.Context(0)
+    split = P.Context(0)
+    split.set_kernel_policy("unfused")
+    pf = P.PreparedPlan(g, devices=dev, ctx=fused)
+    ps = P.PreparedPlan(g, devices=dev, ctx=split)
+    assert [k for k, _, _ in pf.profile()][-2:] == ["fused", "d2h"]
+    assert "wave" in [k for k, _, _ in ps.profile()]
+    pf.launch()
+    ps.launch()
+    a, b = pf.fetch(), ps.fetch()
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
+    c = P.plan(g, dev, ctx=fused)
+    assert list(c.indices) == list(a.indices) and c.cost == a.cost
+
+
+def test_fused_random_graphs(gpu):
+    import paper_1802_04924_b200 as P
+
+    split = P.Context(0)
+    split.set_kernel_policy("unfused")
+    for seed in range(30):
+        g, t = P.random_series_parallel_graph(seed, 5 + seed * 7, 3, 0.4, 4, ctx=gpu.ctx)
+        cat, node, _, _, xfer = t.download()
+        t2 = P.upload_cost_tables(g, cat, node, xfer, split)
+        a, b = P.plan_with_tables(g, t), P.plan_with_tables(g, t2)
+        assert list(a.indices) == list(b.indices) and a.cost == b.cost
