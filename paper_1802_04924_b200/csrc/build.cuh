@@ -109,7 +109,10 @@ __device__ inline int64_t xfer_maxvol_uniform(const EdgeDev &E, const int *cs, c
 }
 
 __device__ inline void xfer_cell(const BuildArgs &a, const EdgeDev &E, int64_t cell) {
-  const int i = static_cast<int>(cell / E.nv), j = static_cast<int>(cell - static_cast<int64_t>(i) * E.nv);
+  // cells are walked destination-config-major (consecutive threads share c_dst, so the
+  // q loop has the same trip count across a warp); the table stays row-major [i][j]
+  const int j = static_cast<int>(cell / E.nu), i = static_cast<int>(cell - static_cast<int64_t>(j) * E.nu);
+  const int64_t out = E.out_off + static_cast<int64_t>(i) * E.nv + j;
   const int64_t *cs64 = a.cfg + 4 * (E.cat_u + i);
   const int64_t *cd64 = a.cfg + 4 * (E.cat_v + j);
   int cs[4], cd[4], ss[4], dpiece[4], spiece[4];
@@ -127,7 +130,7 @@ __device__ inline void xfer_cell(const BuildArgs &a, const EdgeDev &E, int64_t c
   if (a.bw_uniform > 0.0) {
     const int64_t maxvol = xfer_maxvol_uniform(E, cs, cd, ss, spiece, dpiece, band);
     if (maxvol > 0) seconds = 4.0 * static_cast<double>(maxvol) / a.bw_uniform;
-    a.xfer[E.out_off + cell] = seconds;
+    a.xfer[out] = seconds;
     return;
   }
   int dig[4] = {0, 0, 0, 0};
@@ -166,7 +169,7 @@ __device__ inline void xfer_cell(const BuildArgs &a, const EdgeDev &E, int64_t c
     }
   }
   if (a.bw_uniform > 0.0 && maxvol > 0) seconds = 4.0 * static_cast<double>(maxvol) / a.bw_uniform;
-  a.xfer[E.out_off + cell] = seconds;
+  a.xfer[out] = seconds;
 }
 
 } // namespace pp
