@@ -147,6 +147,15 @@ pp_status pp_context_set_precision(pp_context *ctx, int32_t policy);
 /* 0 (default): large certified fixed-point folds use the S16x2 min-plus
  * kernel; 1: every fold uses the generic tiled kernel (for parity checks). */
 pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy);
+/* Multi-GPU: one process per GPU.  Rank 0 creates a 128-byte NCCL unique id,
+ * the caller broadcasts it (e.g. torch.distributed), every rank attaches.  A
+ * context with nranks > 1 row-shards every plan: derived tables are split by
+ * the rows of their source configs, folds compute only local rows, derived t2
+ * operands are all-gathered over NVLink at re-association points, and the final
+ * tables + argmins are all-gathered so every rank returns the same plan.
+ * NCCL is loaded at run time (libnccl.so.2); no link-time dependency. */
+pp_status pp_comm_unique_id(void *id128);
+pp_status pp_context_attach_comm(pp_context *ctx, int32_t nranks, int32_t rank, const void *id128);
 /* kernel launches issued on this context since creation */
 pp_status pp_context_launch_count(const pp_context *ctx, int64_t *launches);
 

@@ -86,6 +86,8 @@ _SIGS = {
     "pp_context_destroy": (C.c_int, [_vp]),
     "pp_context_set_precision": (C.c_int, [_vp, C.c_int32]),
     "pp_context_set_kernel_policy": (C.c_int, [_vp, C.c_int32]),
+    "pp_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "pp_context_attach_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_char_p]),
     "pp_context_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "pp_graph_create": (C.c_int, [C.POINTER(_GraphDesc), _pp]),
     "pp_graph_builtin": (C.c_int, [C.c_char_p, C.c_int64, _pp]),
@@ -164,6 +166,13 @@ def _ptr(a: Optional[np.ndarray]) -> Optional[int]:
     return None if a is None else a.ctypes.data
 
 
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().pp_comm_unique_id(buf))
+    return buf.raw
+
+
 def device_count() -> int:
     n = C.c_int32()
     _check(lib().pp_device_count(C.byref(n)))
@@ -199,6 +208,10 @@ class Context:
         wave; 'generic_unfused': both."""
         _check(lib().pp_context_set_kernel_policy(
             self.h, {"auto": 0, "generic": 1, "unfused": 2, "generic_unfused": 3}[policy]))
+
+    def attach_comm(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        """Join an NCCL communicator: plans on this context are row-sharded across ranks."""
+        _check(lib().pp_context_attach_comm(self.h, nranks, rank, unique_id))
 
     @property
     def launches(self) -> int:
@@ -564,7 +577,7 @@ class PreparedPlan:
         _check(lib().pp_plan_profile(self.h, n.value, _ptr(ms), _ptr(kind), _ptr(work), C.byref(n)))
         names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h", 5: "memset", 6: "mp_reduce",
                  7: "mp_pack", 8: "mp_fold", 9: "mp_rescan", 10: "fused", 11: "fused.tables",
-                 12: "fused.wave", 13: "fused.enumerate", 14: "fused.finish"}
+                 12: "fused.wave", 13: "fused.enumerate", 14: "fused.finish", 15: "allgather"}
         return [(names[int(k)], float(m), float(w)) for k, m, w in zip(kind, ms, work)]
 
     def __del__(self):

@@ -105,6 +105,9 @@ struct pp_context {
   int precision = PP_PRECISION_AUTO;
   bool no_minplus = false; // kernel policy bit 0: generic tiled fold only (parity tests)
   bool no_fused = false;   // kernel policy bit 1: one launch per wave instead of the fused kernel
+  // multi-GPU (pp_context_attach_comm): plans are row-sharded across the ranks
+  void *comm = nullptr; // ncclComm_t
+  int nranks = 1, rank = 0;
   int64_t launches = 0;
   pp::DBuf<unsigned char> desc;  // device image of the current call's descriptors
   pp::PinnedBuf staging;         // pinned host side of desc + results
@@ -121,6 +124,12 @@ struct pp_context {
 };
 
 namespace pp {
+// comm.cu
+void comm_destroy(pp_context *ctx);
+void all_gather(pp_context *ctx, const void *send, void *recv, size_t bytes, cudaStream_t st);
+void group_start();
+void group_end();
+
 inline void check_launch(pp_context *ctx, int n = 1) {
   PP_CUDA(cudaGetLastError());
   ctx->launches += n;

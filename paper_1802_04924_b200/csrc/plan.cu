@@ -120,32 +120,70 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   for (const Op &op : s.ops)
     if (!op.type) PP_REQUIRE(t.counts[static_cast<size_t>(op.removed)] <= 65535, "argmin index exceeds 16 bits");
 
+  // ---- row sharding across ranks (pp_context_attach_comm) --------------------
+  // Every derived table is split by rows (= configs of its source node) into
+  // NR blocks of blk rows; rank RK computes and stores rows [RK*blk, ...).
+  // Original tables are replicated.  A fold needs its t2 in full: a derived t2
+  // is all-gathered first (the re-association points); at the end the final
+  // edges and every argmin table are all-gathered so every rank enumerates and
+  // unwinds identically.
+  const int NR = ctx->comm ? ctx->nranks : 1, RK = ctx->comm ? ctx->rank : 0;
+  const bool shard = NR > 1;
+  auto blk = [&](int id) { return (rows[static_cast<size_t>(id)] + NR - 1) / NR; };
+  auto lr0 = [&](int id) { return std::min(rows[static_cast<size_t>(id)], RK * blk(id)); };
+  auto lrows = [&](int id) {
+    return std::max(0, std::min(rows[static_cast<size_t>(id)], (RK + 1) * blk(id)) - lr0(id));
+  };
+
   // ---- memory plan ----------------------------------------------------------
   auto cells = [&](int id) { return static_cast<size_t>(rows[static_cast<size_t>(id)]) * cols[static_cast<size_t>(id)]; };
+  auto store_cells = [&](int id) { // storage of a derived table on this rank
+    return shard ? static_cast<size_t>(blk(id)) * cols[static_cast<size_t>(id)] : cells(id);
+  };
+  auto full_cells = [&](int id) { // all-gather target (NR padded blocks)
+    return static_cast<size_t>(NR) * blk(id) * cols[static_cast<size_t>(id)];
+  };
   size_t derived_total = 0;
-  for (const Op &op : s.ops) derived_total += align256(cells(op.ne) * sizeof(T));
+  for (const Op &op : s.ops) derived_total += align256(store_cells(op.ne) * sizeof(T));
   const bool keep_all = derived_total <= (size_t(4) << 30);
   OffsetPlanner tab_plan;
   std::vector<size_t> tab_off(static_cast<size_t>(E_total), 0), am_off(s.ops.size(), 0);
-  size_t am_bytes = 0;
+  std::vector<size_t> amfull_off(s.ops.size(), 0), gat_off(static_cast<size_t>(E_total), SIZE_MAX);
+  size_t am_bytes = 0, amfull_bytes = 0, gat_bytes = 0;
   for (int w = 1; w <= s.n_waves; ++w) {
     const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
     for (int x = x0; x < x1; ++x) {
       const int oi = s.exec[static_cast<size_t>(x)];
       const Op &op = s.ops[static_cast<size_t>(oi)];
-      tab_off[static_cast<size_t>(op.ne)] = tab_plan.alloc(cells(op.ne) * sizeof(T));
+      tab_off[static_cast<size_t>(op.ne)] = tab_plan.alloc(store_cells(op.ne) * sizeof(T));
       if (!op.type) {
         am_off[static_cast<size_t>(oi)] = am_bytes;
-        am_bytes += align256(cells(op.ne) * 2);
+        am_bytes += align256(store_cells(op.ne) * 2);
+        if (shard) {
+          amfull_off[static_cast<size_t>(oi)] = amfull_bytes;
+          amfull_bytes += align256(full_cells(op.ne) * 2);
+          if (op.e2 >= t.ne) { // derived t2: gathered in full before the fold
+            gat_off[static_cast<size_t>(op.e2)] = gat_bytes;
+            gat_bytes += align256(full_cells(op.e2) * sizeof(T));
+          }
+        }
       }
     }
     if (!keep_all)
       for (int x = x0; x < x1; ++x) {
         const Op &op = s.ops[static_cast<size_t>(s.exec[static_cast<size_t>(x)])];
         for (int in : {op.e1, op.e2})
-          if (in >= t.ne) tab_plan.release(tab_off[static_cast<size_t>(in)], cells(in) * sizeof(T));
+          if (in >= t.ne) tab_plan.release(tab_off[static_cast<size_t>(in)], store_cells(in) * sizeof(T));
       }
   }
+  if (shard)
+    for (int id : s.final_edges)
+      if (id >= t.ne && gat_off[static_cast<size_t>(id)] == SIZE_MAX) {
+        gat_off[static_cast<size_t>(id)] = gat_bytes;
+        gat_bytes += align256(full_cells(id) * sizeof(T));
+      }
+  // rows of a fold's t1 / a merge's operands this rank works on
+  auto nu_eff = [&](int id) { return shard ? lrows(id) : rows[static_cast<size_t>(id)]; };
   // ---- large fixed-point folds: span certificate + per-wave scratch -----------
   // Span bounds per table (rows: max over rows of max-min; cols likewise),
   // propagated through the log: fold R(out) <= R(t2), K(out) <= K(t1);
@@ -184,7 +222,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         const int oi = s.exec[static_cast<size_t>(x)];
         if (!large[static_cast<size_t>(oi)]) continue;
         const Op &op = s.ops[static_cast<size_t>(oi)];
-        tiles += static_cast<int64_t>((rows[static_cast<size_t>(op.e1)] + kMpTile - 1) / kMpTile) *
+        tiles += static_cast<int64_t>((nu_eff(op.e1) + kMpTile - 1) / kMpTile) *
                  ((cols[static_cast<size_t>(op.e2)] + kMpTile - 1) / kMpTile);
       }
       const int64_t want = std::max<int64_t>(1, (2 * int64_t(ctx->sms) + tiles - 1) / std::max<int64_t>(1, tiles));
@@ -194,8 +232,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         if (!large[static_cast<size_t>(oi)]) continue;
         const Op &op = s.ops[static_cast<size_t>(oi)];
         MpLayout &L = mpl[static_cast<size_t>(oi)];
-        const int nu = rows[static_cast<size_t>(op.e1)], nw = t.counts[static_cast<size_t>(op.removed)],
+        const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)],
                   nv = cols[static_cast<size_t>(op.e2)];
+        if (nu == 0) continue; // no rows of this fold on this rank
         L.nup = (nu + kMpTile - 1) / kMpTile * kMpTile;
         L.nvp = (nv + kMpTile - 1) / kMpTile * kMpTile;
         L.nwp = (nw + kMpChunk - 1) / kMpChunk * kMpChunk;
@@ -226,7 +265,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   const size_t tables_bytes =
       bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
   const size_t off_tables = 0, off_derived = tables_bytes, off_am = off_derived + align256(tab_plan.end()),
-               off_mp = off_am + align256(am_bytes), off_image = off_mp + align256(mp_bytes);
+               off_mp = off_am + align256(am_bytes), off_amfull = off_mp + align256(mp_bytes),
+               off_gat = off_amfull + align256(amfull_bytes), off_image = off_gat + align256(gat_bytes);
 
   // ---- enumeration / unwind descriptors (pointer-free parts) ----------------
   std::vector<int> pos(static_cast<size_t>(t.nl), -1);
@@ -256,10 +296,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     int64_t fold_blocks, red_blocks, pack_blocks, rescan_blocks;
     double mp_cells;
     std::vector<std::pair<int32_t *, size_t>> p_init; // split folds: P <- 0x7f7f7f7f
+    std::vector<std::tuple<const void *, void *, size_t>> gathers; // sharded: derived t2 -> full, before the wave
   };
   struct Image {
     Packer pk;
     std::vector<WaveRange> waves;
+    std::vector<std::tuple<const void *, void *, size_t>> final_gathers; // sharded: final edges + argmins
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
     size_t oG, oT, oFW, oST;
     int nG;
@@ -279,22 +321,33 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     const T *onode = bp ? reinterpret_cast<const T *>(db + off_tables)
                         : (t.mode == kFP64 ? reinterpret_cast<const T *>(t.node.p)
                                            : reinterpret_cast<const T *>(t.node32.p));
+    // this rank's first row of a table (original tables are replicated in full)
+    auto rowp = [&](int id) -> const T * {
+      return id < t.ne && shard ? tabp(id) + static_cast<int64_t>(lr0(id)) * cols[static_cast<size_t>(id)] : tabp(id);
+    };
+    auto gatp = [&](int id) -> T * { return reinterpret_cast<T *>(db + off_gat + gat_off[static_cast<size_t>(id)]); };
+    auto t2p = [&](int id) -> const T * { return shard && id >= t.ne ? gatp(id) : tabp(id); };
+    auto amp = [&](int oi) { return reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]); };
     std::vector<FoldDesc<T>> folds;
     std::vector<MergeDesc<T>> merges;
     std::vector<MpFold> mpf;
     for (int w = 1; w <= s.n_waves; ++w) {
-      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, 0, 0, 0.0, {}};
+      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, 0, 0, 0.0, {}, {}};
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
         T *out = const_cast<T *>(tabp(op.ne));
+        if (shard && !op.type && op.e2 >= t.ne)
+          wr.gathers.emplace_back(tabp(op.e2), gatp(op.e2),
+                                  static_cast<size_t>(blk(op.e2)) * cols[static_cast<size_t>(op.e2)] * sizeof(T));
+        if (nu_eff(op.e1) == 0) continue; // no rows of this op on this rank
         if constexpr (std::is_same_v<T, int32_t>) {
           if (large[static_cast<size_t>(oi)]) {
             const MpLayout &L = mpl[static_cast<size_t>(oi)];
             unsigned char *sb = db + off_mp;
             MpFold f{};
-            f.t1 = tabp(op.e1);
-            f.t2 = tabp(op.e2);
+            f.t1 = rowp(op.e1);
+            f.t2 = t2p(op.e2);
             f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
             f.out = out;
             f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
@@ -305,7 +358,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             f.B16 = reinterpret_cast<uint16_t *>(sb + L.B16);
             f.B16T = reinterpret_cast<uint16_t *>(sb + L.B16T);
             f.P = reinterpret_cast<int32_t *>(sb + L.P);
-            f.nu = rows[static_cast<size_t>(op.e1)];
+            f.nu = nu_eff(op.e1);
             f.nw = t.counts[static_cast<size_t>(op.removed)];
             f.nv = cols[static_cast<size_t>(op.e2)];
             f.nup = L.nup, f.nwp = L.nwp, f.nvp = L.nvp;
@@ -330,12 +383,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         }
         if (!op.type) {
           FoldDesc<T> f;
-          f.t1 = tabp(op.e1);
-          f.t2 = tabp(op.e2);
+          f.t1 = rowp(op.e1);
+          f.t2 = t2p(op.e2);
           f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
           f.out = out;
-          f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
-          f.nu = rows[static_cast<size_t>(op.e1)];
+          f.am = amp(oi);
+          f.nu = nu_eff(op.e1);
           f.nw = t.counts[static_cast<size_t>(op.removed)];
           f.nv = cols[static_cast<size_t>(op.e2)];
           f.tiles_k = (f.nv + kTile - 1) / kTile;
@@ -346,10 +399,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           ++wr.nf;
         } else {
           MergeDesc<T> m;
-          m.a = tabp(op.e1);
-          m.b = tabp(op.e2);
+          m.a = rowp(op.e1);
+          m.b = rowp(op.e2);
           m.out = out;
-          m.n = static_cast<int64_t>(cells(op.ne));
+          m.n = static_cast<int64_t>(nu_eff(op.e1)) * cols[static_cast<size_t>(op.ne)];
           m.blk_begin = wr.mblocks;
           wr.cells += static_cast<double>(m.n);
           wr.mblocks += (m.n + kMergePerBlock - 1) / kMergePerBlock;
@@ -365,9 +418,22 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       en[static_cast<size_t>(d)] = EnumNode{onode + t.cat_off[static_cast<size_t>(l)], t.counts[static_cast<size_t>(l)], 0};
     }
     std::vector<EnumEdge> ee;
-    for (int id : s.final_edges)
-      ee.push_back(EnumEdge{tabp(id), pos[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])],
+    for (int id : s.final_edges) {
+      if (shard && id >= t.ne)
+        im.final_gathers.emplace_back(tabp(id), gatp(id),
+                                      static_cast<size_t>(blk(id)) * cols[static_cast<size_t>(id)] * sizeof(T));
+      ee.push_back(EnumEdge{t2p(id), pos[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])],
                             pos[static_cast<size_t>(s.edst[static_cast<size_t>(id)])], cols[static_cast<size_t>(id)], 0});
+    }
+    auto amfullp = [&](int oi) {
+      return shard ? reinterpret_cast<uint16_t *>(db + off_amfull + amfull_off[static_cast<size_t>(oi)]) : amp(oi);
+    };
+    if (shard)
+      for (size_t oi = 0; oi < s.ops.size(); ++oi)
+        if (!s.ops[oi].type)
+          im.final_gathers.emplace_back(amp(static_cast<int>(oi)), amfullp(static_cast<int>(oi)),
+                                        static_cast<size_t>(blk(s.ops[oi].ne)) *
+                                            cols[static_cast<size_t>(s.ops[oi].ne)] * 2);
     // unwind records grouped by wave, last wave first (kernels.cuh finish_kernel)
     std::vector<UnwindRec> recs;
     std::vector<int32_t> groups{0};
@@ -376,8 +442,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         const int oi = s.exec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
         if (op.type) continue;
-        recs.push_back(UnwindRec{reinterpret_cast<const uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]),
-                                 op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)]});
+        recs.push_back(UnwindRec{amfullp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)]});
       }
       if (static_cast<int32_t>(recs.size()) > groups.back()) groups.push_back(static_cast<int32_t>(recs.size()));
     }
@@ -461,7 +526,22 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->step_work.clear();
   int launches = 0;
   // one cooperative kernel for the whole plan when no fold needs the S16x2 path
-  const bool use_fused = mp_bytes == 0 && !ctx->no_fused;
+  const bool use_fused = mp_bytes == 0 && !ctx->no_fused && !shard;
+  auto push_gathers = [&](const std::vector<std::tuple<const void *, void *, size_t>> &list) {
+    for (size_t g0 = 0; g0 < list.size(); g0 += 256) { // NCCL groups of <= 256 all-gathers
+      std::vector<std::tuple<const void *, void *, size_t>> part(list.begin() + static_cast<long>(g0),
+                                                                 list.begin() + static_cast<long>(std::min(list.size(), g0 + 256)));
+      double bytes = 0.0;
+      for (const auto &x : part) bytes += static_cast<double>(std::get<2>(x)) * NR;
+      P->steps.push_back([ctx, part](cudaStream_t st) {
+        group_start();
+        for (const auto &x : part) all_gather(ctx, std::get<0>(x), std::get<1>(x), std::get<2>(x), st);
+        group_end();
+      });
+      P->step_kind.push_back(15);
+      P->step_work.push_back(bytes);
+    }
+  };
   BuildArgs ba{};
   if (bp) {
     ba.layers = reinterpret_cast<const LayerDev *>(dimg + im.oLay);
@@ -485,6 +565,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   }
   for (const auto &wr : im.waves) {
     if (use_fused) break;
+    push_gathers(wr.gathers);
     if (wr.np > 0) { // large fixed-point folds of this wave: reduce -> pack -> fold -> rescan
       const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + wr.p0;
       const int np = wr.np;
@@ -538,6 +619,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     P->step_work.push_back(wr.cells);
     ++launches;
   }
+  push_gathers(im.final_gathers);
   {
     const EnumNode *en = reinterpret_cast<const EnumNode *>(dimg + im.oN);
     const EnumEdge *ee = reinterpret_cast<const EnumEdge *>(dimg + im.oE);

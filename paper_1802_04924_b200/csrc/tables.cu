@@ -118,6 +118,7 @@ pp_status pp_context_destroy(pp_context *ctx) {
   ctx->desc.release();
   ctx->scratch.release();
   ctx->plan_pool.release();
+  pp::comm_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->stream && !ctx->external_stream) cudaStreamDestroy(ctx->stream);

@@ -1,0 +1,74 @@
+"""Multi-process paths.
+
+* CPU (gloo, world_size 2): the sweep sharding, the global argmin all-gather
+  and the max-over-ranks reduction of paper_1802_04924_b200.distributed.
+* GPU (>= 2 B200s; skipped on a single-GPU box): row-sharded plans over NCCL
+  equal single-GPU plans bit for bit (tests/mgpu_worker.py under torchrun).
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, size, port, q):
+    sys.path.insert(0, ROOT)
+    from paper_1802_04924_b200 import distributed as PD
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    items = list(range(11))
+    mine = PD.shard(items, rank, size)
+    # a fake sweep: cost = (i - 6)^2 with a deliberate tie at i = 4 and i = 8
+    local = [((i - 6) ** 2 if i not in (4, 8) else 1, i, f"plan{i}") for i, _ in mine]
+    best = PD.global_best(local)
+    mx = PD.max_over_ranks(float(rank + 1))
+    q.put((rank, [i for i, _ in mine], best, mx))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sweep_sharding_and_global_argmin_gloo():
+    size, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, size, port, q)) for r in range(size)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(size)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort()
+    covered = sorted(i for _, part, _, _ in out for i in part)
+    assert covered == list(range(11))
+    for _, _, best, mx in out:
+        assert best == (0, 6, "plan6")
+        assert mx == 2.0
+
+
+@pytest.mark.gpu
+def test_row_sharded_plans_match_single_gpu():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = min(torch.cuda.device_count(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", f"--nproc-per-node={n}",
+           os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.stdout.count(": OK") == n
