@@ -39,6 +39,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
 METRIC = "Inception-v3 optimal-config search ms; min-plus cell-updates/s vs FP32 roofline"
 PAPER_MS = 100.0  # PAPER.md:80 "about 100 ms" for Inception-v3 (120 nodes) on 16 GPUs
@@ -295,14 +296,35 @@ def run_ours(args):
 def minplus(P, ctx, args, flush, stream):
     """Config-5 synthetic sweep point: 1000 layers (bp 0.3, seed 1 topology),
     C configs per layer, device-generated dyadic tables, exact int32 DP."""
+    import torch
+
     C = args.minplus_c
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:  # one plan row-sharded across all ranks (NCCL all-gathers at re-association points)
+        from paper_1802_04924_b200 import distributed as PD
+
+        ctx = P.Context(ctx.device, stream=stream.cuda_stream)
+        PD.attach(ctx)
     g = P.series_parallel_graph(1, 1000, 0.3)
     t = P.synthetic_cost_tables(g, C, seed=1, ctx=ctx)
     prep = P.PreparedPlan(g, tables=t, ctx=ctx)
     prep.launch()
     r = prep.fetch()
+    global_cells = float(C) ** 3 * sum(1 for rec in g.schedule()[0] if rec[0] == 0)
     with Clocks(ctx.device) as clk:
         runs = [prep.profile() for _ in range(args.minplus_runs)]
+    # whole-plan device time of one search, max over ranks
+    starts, ends = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    starts.record(stream)
+    prep.launch()
+    ends.record(stream)
+    prep.fetch()
+    plan_ms = starts.elapsed_time(ends)
+    if world > 1:
+        from paper_1802_04924_b200 import distributed as PD
+
+        plan_ms = PD.max_over_ranks(plan_ms, device="cuda")
     folds = [(ms, w) for run in runs for kind, ms, w in run if kind == "mp_fold"]
     if not folds:  # generic path only (no certified large folds)
         folds = [(ms, w) for run in runs for kind, ms, w in run if kind == "wave"]
@@ -326,8 +348,11 @@ def minplus(P, ctx, args, flush, stream):
                      "launches": len(folds) // len(runs),
                      "peak_basis": f"148 SM x 128 FP32 lanes x 2 ops x {f_mhz:.0f} MHz (measured SM clock under load)"},
         "minplus": {"configs": C, "layers": g.n_layers, "cell_updates": cells,
-                    "cell_updates_per_s": cells / (wave_ms * 1e-3), "fold_kernel_ms": wave_ms, "plan_ms": total_ms,
-                    "plan_cell_updates_per_s": cells / (total_ms * 1e-3), "ms_by_kernel": by_kind,
+                    "cell_updates_per_s": cells / (wave_ms * 1e-3), "fold_kernel_ms": wave_ms,
+                    "profiled_plan_ms": total_ms, "ms_by_kernel": by_kind,
+                    "plan_ms": plan_ms, "global_cell_updates": global_cells,
+                    "plan_cell_updates_per_s": global_cells / (plan_ms * 1e-3), "ranks": world,
+                    "sharding": "row blocks of c_u across ranks" if world > 1 else "none",
                     "cost": r.cost, "precision": r.precision, "clocks": c,
                     "workload": f"plan_with_tables(series_parallel(seed 1, 1000 layers, bp 0.3), C={C})"},
     }

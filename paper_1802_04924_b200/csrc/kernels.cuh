@@ -25,7 +25,10 @@ template <class T> struct FoldDesc {
   int32_t nu, nw, nv;
   int32_t tiles_k;    // tiles along nv
   int64_t tile_begin; // first global tile id of this fold
+  int32_t small;      // 1: 16x16 output tiles (one cell per thread) for waves too small to fill the GPU
 };
+
+constexpr int kSmallTile = 16;
 
 template <class T> struct MergeDesc {
   const T *a, *b;
@@ -62,6 +65,59 @@ __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds,
     }
     const FoldDesc<T> f = folds[lo];
     const int64_t tile = b - f.tile_begin;
+    if (f.small) { // 16x16 tile, one cell per thread, two interleaved scans
+      const int i0 = static_cast<int>(tile / f.tiles_k) * kSmallTile;
+      const int k0 = static_cast<int>(tile % f.tiles_k) * kSmallTile;
+      const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+      T be = T(0), bo = T(0);
+      int je = 0, jo = -1;
+      T pa[2], pb[2];
+      auto fetch = [&](int j0) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int idx = threadIdx.x + q * kFoldThreads;
+          const int r = idx >> 5, c = idx & 31; // A: 16 rows x 32 j
+          const int i = i0 + r, j = j0 + c;
+          pa[q] = (i < f.nu && j < f.nw) ? T(f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j]) : T(0);
+          const int jr = idx >> 4, kc = idx & 15; // B: 32 j x 16 cols
+          const int jj = j0 + jr, k = k0 + kc;
+          pb[q] = (jj < f.nw && k < f.nv) ? f.t2[static_cast<int64_t>(jj) * f.nv + k] : T(0);
+        }
+      };
+      fetch(0);
+      for (int j0 = 0; j0 < f.nw; j0 += kTile) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int idx = threadIdx.x + q * kFoldThreads;
+          As[idx >> 5][idx & 31] = pa[q];
+          Bs[idx >> 4][idx & 15] = pb[q];
+        }
+        __syncthreads();
+        if (j0 + kTile < f.nw) fetch(j0 + kTile);
+        const int jn = min(kTile, f.nw - j0);
+        int jj = 0;
+        for (; jj + 1 < jn; jj += 2) {
+          const T c0 = As[ty][jj] + Bs[jj][tx];
+          const T c1 = As[ty][jj + 1] + Bs[jj + 1][tx];
+          const int j = j0 + jj;
+          if (j == 0 || c0 < be) be = c0, je = j;
+          if (jo < 0 || c1 < bo) bo = c1, jo = j + 1;
+        }
+        if (jj < jn) {
+          const T c0 = As[ty][jj] + Bs[jj][tx];
+          const int j = j0 + jj;
+          if (j == 0 || c0 < be) be = c0, je = j;
+        }
+        __syncthreads();
+      }
+      const int i = i0 + ty, k = k0 + tx;
+      if (i < f.nu && k < f.nv) {
+        const bool odd = jo >= 0 && (bo < be || (bo == be && jo < je));
+        f.out[static_cast<int64_t>(i) * f.nv + k] = odd ? bo : be;
+        f.am[static_cast<int64_t>(i) * f.nv + k] = static_cast<uint16_t>(odd ? jo : je);
+      }
+      return;
+    }
     const int i0 = static_cast<int>(tile / f.tiles_k) * kTile;
     const int k0 = static_cast<int>(tile % f.tiles_k) * kTile;
     const int ty = threadIdx.x >> 3, tx = (threadIdx.x & 7) * 4;

@@ -18,6 +18,9 @@
 #include <climits>
 #include <cstring>
 #include <functional>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 
 namespace pp {
@@ -333,6 +336,18 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<MpFold> mpf;
     for (int w = 1; w <= s.n_waves; ++w) {
       WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, 0, 0, 0.0, {}, {}};
+      // a wave whose generic folds cover fewer than 2 x SMs 32x32 tiles uses
+      // 16x16 tiles: 4x the blocks, a quarter of the per-tile latency
+      int64_t big_tiles = 0;
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        if (op.type || large[static_cast<size_t>(oi)]) continue;
+        big_tiles += static_cast<int64_t>((nu_eff(op.e1) + kTile - 1) / kTile) *
+                     ((cols[static_cast<size_t>(op.e2)] + kTile - 1) / kTile);
+      }
+      const bool small_wave = big_tiles < 2 * int64_t(ctx->sms);
+      const int ts = small_wave ? kSmallTile : kTile;
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
@@ -391,10 +406,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           f.nu = nu_eff(op.e1);
           f.nw = t.counts[static_cast<size_t>(op.removed)];
           f.nv = cols[static_cast<size_t>(op.e2)];
-          f.tiles_k = (f.nv + kTile - 1) / kTile;
+          f.small = small_wave ? 1 : 0;
+          f.tiles_k = (f.nv + ts - 1) / ts;
           f.tile_begin = wr.ftiles;
           wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
-          wr.ftiles += static_cast<int64_t>((f.nu + kTile - 1) / kTile) * f.tiles_k;
+          wr.ftiles += static_cast<int64_t>((f.nu + ts - 1) / ts) * f.tiles_k;
           folds.push_back(f);
           ++wr.nf;
         } else {
@@ -692,7 +708,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       int64_t items = std::max<int64_t>(nblk, 1);
       if (bp) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
       for (const auto &wr : im.waves) items = std::max<int64_t>(items, wr.ftiles + wr.mblocks);
-      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, int64_t(ctx->sms) * occ));
+      static const int per_sm_env = std::getenv("PARPLAN_FUSED_BLOCKS_PER_SM")
+                                        ? std::atoi(std::getenv("PARPLAN_FUSED_BLOCKS_PER_SM"))
+                                        : 0;
+      const int per_sm = per_sm_env > 0 ? std::min(per_sm_env, occ) : occ;
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, int64_t(ctx->sms) * per_sm));
       P->steps.push_back([ctx, fz, grid](cudaStream_t st) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
@@ -781,6 +801,8 @@ static void fetch(pp_prepared *P, int32_t *indices, pp_plan_result *res) {
 
 void run_plan(pp_context *ctx, Graph &g, Tables *t, const pp_device_desc *dev, int k_bound, int32_t *indices,
               pp_plan_result *res) {
+  static const bool trace = std::getenv("PARPLAN_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   pp_prepared P;
   P.ctx = ctx;
   P.g = &g;
@@ -788,8 +810,16 @@ void run_plan(pp_context *ctx, Graph &g, Tables *t, const pp_device_desc *dev, i
   P.transient = true;
   PP_CUDA(cudaSetDevice(ctx->device));
   prepare(&P, dev, k_bound);
+  const auto t1 = std::chrono::steady_clock::now();
   launch(&P, true);
+  const auto t2 = std::chrono::steady_clock::now();
   fetch(&P, indices, res);
+  const auto t3 = std::chrono::steady_clock::now();
+  if (trace) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "[parplan] plan: prepare %.1f us, launch %.1f us, fetch %.1f us, image %zu B\n", us(t0, t1),
+                 us(t1, t2), us(t2, t3), P.image_bytes);
+  }
 }
 
 } // namespace pp
