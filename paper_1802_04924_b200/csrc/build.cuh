@@ -24,7 +24,8 @@ __device__ inline void node_cost_cell(const BuildArgs &a, int64_t gi) {
       hi = mid - 1;
   }
   const LayerDev &L = a.layers[lo];
-  const int64_t *c = a.cfg + 4 * gi;
+  const int32_t *c32 = a.cfg + 4 * gi;
+  const int64_t c[4] = {c32[0], c32[1], c32[2], c32[3]};
   const int64_t total = c[0] * c[1] * c[2] * c[3];
   // compute_cost (cost.hpp:60-72)
   const int64_t flops = geo::layer_flops(L.kind, L.params, L.shape, L.in_shape);
@@ -50,6 +51,46 @@ __device__ inline void node_cost_cell(const BuildArgs &a, int64_t gi) {
 // checked on the host); volumes are int64.  Destination partitions q are
 // walked with an odometer over their per-dimension digits (W fastest), so
 // no division sits in the q loop except the O(1) piece lookups.
+// dim_stats (geometry.hpp) with the two divisions by the piece size done as a
+// float multiply by a per-cell reciprocal plus one exact correction (valid
+// for coordinates < 2^22; the host checks tensor extents before choosing it).
+__device__ __forceinline__ int div_fast(int a, int P, float rcp) {
+  int x = __float2int_rz(__int2float_rn(a) * rcp);
+  if (x * P > a) --x;
+  else if ((x + 1) * P <= a) ++x;
+  return x;
+}
+
+__device__ __forceinline__ geo::DimStats<int> dim_stats_fast(int a, int b, int P, float rcp) {
+  geo::DimStats<int> s{0, 0, 0, false};
+  if (b <= a) return s;
+  const int x0 = div_fast(a, P, rcp), x1 = div_fast(b - 1, P, rcp);
+  if (x0 == x1) {
+    s.best = b - a, s.arg = x0, s.unique = true, s.second = 0;
+    return s;
+  }
+  const int o0 = (x0 + 1) * P - a, o1 = b - x1 * P;
+  if (x1 == x0 + 1) {
+    if (o0 == o1) {
+      s.best = s.second = o0, s.unique = false;
+    } else {
+      s.unique = true;
+      s.best = o0 > o1 ? o0 : o1;
+      s.second = o0 > o1 ? o1 : o0;
+      s.arg = o0 > o1 ? x0 : x1;
+    }
+    return s;
+  }
+  const int full = (x1 - x0 - 1) + (o0 == P) + (o1 == P);
+  s.best = P;
+  if (full >= 2) {
+    s.second = P, s.unique = false;
+  } else {
+    s.unique = true, s.arg = x0 + 1, s.second = o0 > o1 ? o0 : o1;
+  }
+  return s;
+}
+
 // Uniform bandwidth (the common case): seconds = RN(4 * maxvol / bw) with
 // maxvol = max over destination partitions q (non-empty need) of
 // max_{p != q} vol(owned(p) ∩ need_q).  Each dimension's need interval
@@ -65,6 +106,9 @@ __device__ inline int64_t xfer_maxvol_uniform(const EdgeDev &E, const int *cs, c
   for (int k = 0; k < 7; ++k) par[k] = static_cast<int>(E.params[k]);
   int dig[4] = {0, 0, 0, 0};
   geo::DimStats<int> st[4];
+  float rcp[4];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) rcp[d] = 1.0f / static_cast<float>(spiece[d]);
   int64_t maxvol = 0;
   int changed = 0;
   for (int q = 0; q < td; ++q) {
@@ -75,7 +119,7 @@ __device__ inline int64_t xfer_maxvol_uniform(const EdgeDev &E, const int *cs, c
       geo::required_box_owned<int, int>(kind, par, ss, band, olo, ohi, lo, hi);
 #pragma unroll
       for (int d = 0; d < 4; ++d)
-        if (d >= changed) st[d] = geo::dim_stats<int>(lo[d], hi[d], spiece[d]);
+        if (d >= changed) st[d] = dim_stats_fast(lo[d], hi[d], spiece[d], rcp[d]);
     }
     // combine (geometry.hpp: max_offdiag_volume)
     const int64_t M = static_cast<int64_t>(st[0].best) * st[1].best * st[2].best * st[3].best;
@@ -113,8 +157,8 @@ __device__ inline void xfer_cell(const BuildArgs &a, const EdgeDev &E, int64_t c
   // q loop has the same trip count across a warp); the table stays row-major [i][j]
   const int j = static_cast<int>(cell / E.nu), i = static_cast<int>(cell - static_cast<int64_t>(j) * E.nu);
   const int64_t out = E.out_off + static_cast<int64_t>(i) * E.nv + j;
-  const int64_t *cs64 = a.cfg + 4 * (E.cat_u + i);
-  const int64_t *cd64 = a.cfg + 4 * (E.cat_v + j);
+  const int32_t *cs64 = a.cfg + 4 * (E.cat_u + i);
+  const int32_t *cd64 = a.cfg + 4 * (E.cat_v + j);
   int cs[4], cd[4], ss[4], dpiece[4], spiece[4];
 #pragma unroll
   for (int d = 0; d < 4; ++d) {

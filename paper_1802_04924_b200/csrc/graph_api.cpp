@@ -38,6 +38,15 @@ const Schedule &Graph::schedule() {
   return *sched;
 }
 
+const Graph::Catalogs &Graph::catalogs(int devices) const {
+  auto it = catalog_cache.find(devices);
+  if (it != catalog_cache.end()) return it->second;
+  Catalogs c;
+  enumerate_catalogs(*this, devices, &c.counts, &c.configs);
+  c.configs32.assign(c.configs.begin(), c.configs.end());
+  return catalog_cache.emplace(devices, std::move(c)).first->second;
+}
+
 void enumerate_catalogs(const Graph &g, int devices, std::vector<int32_t> *counts, std::vector<int64_t> *configs) {
   counts->clear();
   configs->clear();

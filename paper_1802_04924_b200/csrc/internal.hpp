@@ -8,6 +8,7 @@
 #include "parplan/partition.hpp"
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -67,9 +68,18 @@ struct Graph {
   std::vector<int> esrc, edst, epos, rank;
   std::vector<int64_t> band_offset; // per edge, Concat destinations
   std::unique_ptr<Schedule> sched;  // lazily built, topology-only
+  // enumerate_configs of every layer for a device count (pure function of the
+  // immutable graph and D): counts, configs (4 x int64), configs (4 x int32)
+  struct Catalogs {
+    std::vector<int32_t> counts;
+    std::vector<int64_t> configs;
+    std::vector<int32_t> configs32;
+  };
+  mutable std::map<int, Catalogs> catalog_cache;
 
   explicit Graph(parplan::ComputationGraph cg);
   const Schedule &schedule();
+  const Catalogs &catalogs(int devices) const;
 };
 
 // Catalogs of every layer (enumerate_configs) flattened: counts + 4 int64 each.

@@ -315,6 +315,10 @@ struct FinishArgs {
   const int32_t *group_begin;
   int n_groups;
   double *terms; // [nl + ne] scratch
+  // optional zero-copy of the result block (indices, digits, final cost, cost)
+  unsigned char *host_res;
+  const unsigned char *dev_res;
+  size_t res_bytes; // multiple of 4
   int32_t *indices;
   int nl;
   const void *onode, *oxfer;
@@ -401,6 +405,12 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
     double t = 0.0;
     for (int x = 0; x < a.nl + a.ne; ++x) t += a.terms[x];
     *a.cost = t;
+  }
+  if (a.host_res) { // zero-copy: results straight into pinned host memory
+    __syncthreads();
+    for (size_t b = threadIdx.x; b < a.res_bytes / 4; b += kFinishThreads)
+      reinterpret_cast<volatile uint32_t *>(a.host_res)[b] = reinterpret_cast<const uint32_t *>(a.dev_res)[b];
+    __threadfence_system();
   }
 }
 

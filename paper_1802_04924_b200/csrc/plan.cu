@@ -490,7 +490,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     if (bp) {
       im.oLay = pk.put(bp->L);
       im.oEdg = pk.put(bp->E);
-      im.oCfg = pk.put(t.configs);
+      im.oCfg = pk.put(bp->cfg32);
       im.oRat = pk.put(bp->rates);
       im.oBw = pk.put(bp->bw);
     }
@@ -505,22 +505,30 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   };
 
   // sizes (pointer values do not change the layout)
-  const size_t image_bytes = make_image(nullptr).pk.size();
-  const size_t total = off_image + align256(image_bytes);
+  // The image holds absolute device pointers, so it is built against the final
+  // base.  One-shot plans reuse the context pool: build against the current
+  // pool and rebuild only when the pool has to grow (first calls).
+  Image im;
   if (P->transient) {
-    ctx->plan_pool.ensure(total);
+    im = make_image(ctx->plan_pool.p);
+    const size_t total = off_image + align256(im.pk.size());
+    if (total > ctx->plan_pool.n || !ctx->plan_pool.p) {
+      ctx->plan_pool.ensure(total + total / 4);
+      im = make_image(ctx->plan_pool.p);
+    }
     P->dbase = ctx->plan_pool.p;
-    P->hbase = static_cast<unsigned char *>(ctx->plan_pinned.ensure(align256(image_bytes)));
+    P->hbase = static_cast<unsigned char *>(ctx->plan_pinned.ensure(align256(im.pk.size())));
   } else {
+    const size_t total = off_image + align256(make_image(nullptr).pk.size());
     P->dmem.alloc(total);
     P->dbase = P->dmem.p;
     // poison: a slot the device work fails to write shows up as garbage
     PP_CUDA(cudaMemsetAsync(P->dbase, 0xFF, total, ctx->stream));
-    P->hbase = static_cast<unsigned char *>(P->hmem.ensure(align256(image_bytes)));
+    im = make_image(P->dbase);
+    P->hbase = static_cast<unsigned char *>(P->hmem.ensure(align256(im.pk.size())));
   }
   unsigned char *db = P->dbase;
   unsigned char *dimg = db + off_image;
-  Image im = make_image(db);
   std::memcpy(P->hbase, im.pk.bytes.data(), im.pk.size());
   P->image_off = off_image;
   P->image_bytes = im.pk.size();
@@ -562,7 +570,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   if (bp) {
     ba.layers = reinterpret_cast<const LayerDev *>(dimg + im.oLay);
     ba.edges = reinterpret_cast<const EdgeDev *>(dimg + im.oEdg);
-    ba.cfg = reinterpret_cast<const int64_t *>(dimg + im.oCfg);
+    ba.cfg = reinterpret_cast<const int32_t *>(dimg + im.oCfg);
     ba.rates = reinterpret_cast<const double *>(dimg + im.oRat);
     ba.bw = reinterpret_cast<const double *>(dimg + im.oBw);
     ba.node = t.node.p, ba.compute = t.compute.p, ba.sync = t.sync.p, ba.xfer = t.xfer64.p;
@@ -678,6 +686,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.edst = reinterpret_cast<const int32_t *>(dimg + im.oD);
     fa.counts = reinterpret_cast<const int32_t *>(dimg + im.oC);
     fa.ne = t.ne;
+    fa.host_res = P->hbase + P->res_off;
+    fa.dev_res = dimg + P->res_off;
+    fa.res_bytes = (P->res_bytes + 3) & ~size_t(3);
     if (!use_fused) {
       P->steps.push_back([ctx, fa](cudaStream_t st) {
         finish_kernel<T><<<1, kFinishThreads, 0, st>>>(fa);
@@ -731,13 +742,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       launches += 1;
     }
   }
-  unsigned char *hres = P->hbase + P->res_off, *dres = dimg + P->res_off;
-  const size_t rb = P->res_bytes;
-  P->steps.push_back([hres, dres, rb](cudaStream_t st) {
-    PP_CUDA(cudaMemcpyAsync(hres, dres, rb, cudaMemcpyDeviceToHost, st));
-  });
-  P->step_kind.push_back(4);
-  P->step_work.push_back(static_cast<double>(rb));
+  // results reach the host by zero-copy stores at the end of the finish phase
+  // (FinishArgs::host_res), so no D2H copy node follows
   P->launches_per_run = launches;
 }
 

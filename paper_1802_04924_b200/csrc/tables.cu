@@ -325,7 +325,7 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
     t.ctx = ctx;
     const BuildPlan bp = plan_build(t, gh->impl, dev);
     Packer pk;
-    const size_t oL = pk.put(bp.L), oE = pk.put(bp.E), oC = pk.put(t.configs);
+    const size_t oL = pk.put(bp.L), oE = pk.put(bp.E), oC = pk.put(bp.cfg32);
     const size_t oR = pk.put(dev->compute_rates, static_cast<size_t>(bp.D));
     const size_t oB = pk.put(dev->bandwidth, static_cast<size_t>(bp.D) * bp.D);
     t.node.alloc(static_cast<size_t>(t.ncells));
@@ -337,7 +337,7 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
     BuildArgs a;
     a.layers = reinterpret_cast<const LayerDev *>(base + oL);
     a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
-    a.cfg = reinterpret_cast<const int64_t *>(base + oC);
+    a.cfg = reinterpret_cast<const int32_t *>(base + oC);
     a.rates = reinterpret_cast<const double *>(base + oR);
     a.bw = reinterpret_cast<const double *>(base + oB);
     a.node = t.node.p, a.compute = t.compute.p, a.sync = t.sync.p, a.xfer = t.xfer64.p;
@@ -369,16 +369,20 @@ BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev) {
                                 std::vector<double>(dev->bandwidth, dev->bandwidth + static_cast<size_t>(D) * D));
   for (int l = 0; l < g.nl; ++l) { // K1 runs its region arithmetic on int32 coordinates
     const int64_t *s = &g.shape[static_cast<size_t>(l) * 4];
-    PP_REQUIRE(s[1] * s[2] * s[3] < (int64_t(1) << 31) && s[0] < (int64_t(1) << 31),
-               "layer '" + g.g.layer(l).id + "': tensor extents exceed the int32 range of the table builder");
+    // K1 divides coordinates by piece sizes with a float reciprocal + exact
+    // correction, valid below 2^22 (build.cuh: div_fast)
+    PP_REQUIRE(s[1] * s[2] * s[3] < (int64_t(1) << 22) && s[0] < (int64_t(1) << 22),
+               "layer '" + g.g.layer(l).id + "': tensor extents exceed the 2^22 range of the table builder");
   }
-  std::vector<int32_t> counts;
-  enumerate_catalogs(g, D, &counts, &t.configs);
+  const Graph::Catalogs &cats = g.catalogs(D); // cached per (graph, D)
+  const std::vector<int32_t> &counts = cats.counts;
+  t.configs = cats.configs;
   init_layout(t, g, counts);
   t.mode = kFP64;
   t.analytic = true;
   BuildPlan bp;
   bp.D = D;
+  bp.cfg32 = cats.configs32;
 
   double bw_uniform = dev->bandwidth[D > 1 ? 1 : 0];
     for (int p = 0; p < D; ++p)

@@ -63,7 +63,7 @@ struct EdgeDev {
 struct BuildArgs {
   const LayerDev *layers;
   const EdgeDev *edges;
-  const int64_t *cfg; // 4 per config
+  const int32_t *cfg; // 4 per config (degrees <= device count)
   const double *rates;
   const double *bw; // D*D
   double *node, *compute, *sync, *xfer;
@@ -80,6 +80,7 @@ struct BuildPlan {
   double bw_uniform = 0.0;
   int D = 0;
   std::vector<double> rates, bw; // the device graph, for plans that embed it
+  std::vector<int32_t> cfg32;    // catalogs as the kernels read them
 };
 
 // Fills t's layout (catalogs, offsets; FP64 analytic mode, no allocation) and

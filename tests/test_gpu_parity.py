@@ -111,7 +111,7 @@ def test_prepared_plan_and_profile(gpu):
         assert list(r.indices) == list(want.indices) and r.cost == want.cost
     prof = prep.profile()
     kinds = [k for k, _, _ in prof]
-    assert kinds[0] == "fused.tables" and kinds.count("fused.wave") == r.waves and kinds[-2:] == ["fused", "d2h"]
+    assert kinds[0] == "fused.tables" and kinds.count("fused.wave") == r.waves and kinds[-1] == "fused"
     assert sum(w for k, _, w in prof if k == "fused.wave") > 0
 
 
@@ -160,7 +160,7 @@ def test_fused_and_per_wave_executors_agree(gpu, model, D):
     split.set_kernel_policy("unfused")
     pf = P.PreparedPlan(g, devices=dev, ctx=fused)
     ps = P.PreparedPlan(g, devices=dev, ctx=split)
-    assert [k for k, _, _ in pf.profile()][-2:] == ["fused", "d2h"]
+    assert [k for k, _, _ in pf.profile()][-1] == "fused"
     assert "wave" in [k for k, _, _ in ps.profile()]
     pf.launch()
     ps.launch()
