@@ -13,7 +13,7 @@ namespace geo = parplan::geo;
 
 constexpr int kBuildThreads = 128;
 
-__device__ inline void node_cost_cell(const BuildArgs &a, int64_t gi) {
+__device__ __forceinline__ void node_cost_cell(const BuildArgs &a, int64_t gi) {
   // layer with cat_off <= gi < cat_off + count (binary search)
   int lo = 0, hi = a.nl - 1;
   while (lo < hi) {
@@ -47,10 +47,6 @@ __device__ inline void node_cost_cell(const BuildArgs &a, int64_t gi) {
   a.node[gi] = tc + ts;
 }
 
-// One (c_src, c_dst) cell.  Coordinates are int32 (tensor extents < 2^31,
-// checked on the host); volumes are int64.  Destination partitions q are
-// walked with an odometer over their per-dimension digits (W fastest), so
-// no division sits in the q loop except the O(1) piece lookups.
 // dim_stats (geometry.hpp) with the two divisions by the piece size done as a
 // float multiply by a per-cell reciprocal plus one exact correction (valid
 // for coordinates < 2^22; the host checks tensor extents before choosing it).
@@ -91,129 +87,229 @@ __device__ __forceinline__ geo::DimStats<int> dim_stats_fast(int a, int b, int P
   return s;
 }
 
-// Uniform bandwidth (the common case): seconds = RN(4 * maxvol / bw) with
-// maxvol = max over destination partitions q (non-empty need) of
-// max_{p != q} vol(owned(p) ∩ need_q).  Each dimension's need interval
-// depends on one destination digit only (flatten: dims 1-3 on digit 1), so
-// when the odometer advances digit d only dims d..3 get new overlap stats:
-// ~1.1 dim_stats per q instead of 4.
-__device__ inline int64_t xfer_maxvol_uniform(const EdgeDev &E, const int *cs, const int *cd, const int *ss,
-                                              const int *spiece, const int *dpiece, int band) {
-  const int td = cd[0] * cd[1] * cd[2] * cd[3];
-  const int kind = E.kind;
-  int par[7];
-#pragma unroll
-  for (int k = 0; k < 7; ++k) par[k] = static_cast<int>(E.params[k]);
-  int dig[4] = {0, 0, 0, 0};
-  geo::DimStats<int> st[4];
+// Geometry of one (c_src, c_dst) cell.  Coordinates are int32 (tensor
+// extents < 2^22, checked on the host); volumes are int64.  Cells are walked
+// destination-config-major (consecutive threads share c_dst); the table
+// stays row-major [i][j].
+struct XferCell {
+  int cs[4], cd[4], ss[4], spiece[4], dpiece[4];
   float rcp[4];
+  int par[7];
+  int band, kind;
+  int64_t out;
+};
+
+__device__ __forceinline__ void xfer_decode(const BuildArgs &a, const EdgeDev &E, int64_t cell, XferCell &c) {
+  const int j = static_cast<int>(cell / E.nu), i = static_cast<int>(cell - static_cast<int64_t>(j) * E.nu);
+  c.out = E.out_off + static_cast<int64_t>(i) * E.nv + j;
+  const int32_t *cs32 = a.cfg + 4 * (E.cat_u + i);
+  const int32_t *cd32 = a.cfg + 4 * (E.cat_v + j);
 #pragma unroll
-  for (int d = 0; d < 4; ++d) rcp[d] = 1.0f / static_cast<float>(spiece[d]);
+  for (int d = 0; d < 4; ++d) {
+    c.cs[d] = cs32[d];
+    c.cd[d] = cd32[d];
+    c.ss[d] = static_cast<int>(E.sshape[d]);
+    c.spiece[d] = c.ss[d] / c.cs[d];
+    c.dpiece[d] = static_cast<int>(E.dshape[d]) / c.cd[d];
+    c.rcp[d] = 1.0f / static_cast<float>(c.spiece[d]);
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) c.par[k] = static_cast<int>(E.params[k]);
+  c.band = static_cast<int>(E.band);
+  c.kind = E.kind;
+}
+
+// Dimension d of required_box_owned (geometry.hpp) for an owned interval
+// [olo, ohi) along d.  Every kind but Flatten maps each dimension of the
+// need box from the same dimension of the owned box alone.
+__device__ __forceinline__ void need_interval(const XferCell &c, int d, int olo, int ohi, int *lo, int *hi) {
+  *lo = olo, *hi = ohi;
+  switch (c.kind) {
+  case geo::kConcat:
+    if (d == c.par[0]) {
+      int l = geo::imax<int>(olo, c.band), h = geo::imin<int>(ohi, c.band + c.ss[d]);
+      if (h < l) h = l;
+      *lo = l - c.band, *hi = h - c.band;
+    }
+    return;
+  case geo::kSoftmax:
+    return;
+  case geo::kConv:
+    if (d == 1) *lo = 0, *hi = c.ss[1];
+    if (d == 2) geo::window<int>(olo, ohi, c.par[1], c.par[3], c.par[5], c.ss[2], lo, hi);
+    if (d == 3) geo::window<int>(olo, ohi, c.par[2], c.par[4], c.par[6], c.ss[3], lo, hi);
+    return;
+  case geo::kPool:
+    if (d == 2) geo::window<int>(olo, ohi, c.par[0], c.par[2], c.par[4], c.ss[2], lo, hi);
+    if (d == 3) geo::window<int>(olo, ohi, c.par[1], c.par[3], c.par[5], c.ss[3], lo, hi);
+    return;
+  case geo::kFC:
+    if (d > 0) *lo = 0, *hi = c.ss[d];
+    return;
+  default:
+    if (d > 0) *lo = 0, *hi = 0;
+    return;
+  }
+}
+
+// Uniform bandwidth (the common case): seconds = RN(4 * maxvol / bw) with
+// maxvol = max over destination partitions q of max_{p != q} vol(owned(p) ∩
+// need_q) (cost.hpp:103-131).  With M(q) = prod_d best_d(q_d) the per-q
+// maximum over all p, M is separable, so Mmax = prod_d max_x best_d(x) costs
+// sum_d cd[d] dim_stats instead of prod_d cd[d].  Mmax is the answer unless
+// every q attaining it has a unique maximiser p* equal to q itself; writing
+// p* - q = sum_d delta_d(q_d) with delta_d(x) = arg_d(x) * S_d - x * D_d
+// (S, D the flat strides of the two configs), some maximising q has p* != q
+// iff a maximising digit has non-unique stats, or delta varies over the
+// maximising digits of some dimension, or the constant deltas do not sum to
+// 0.  Returns -1 when no such q exists (the diagonal cells) or the kind is
+// Flatten; those cells take xfer_maxvol_walk.
+__device__ __forceinline__ int64_t xfer_maxvol_separable(const XferCell &c) {
+  if (c.kind == geo::kFlatten) return -1;
+  int64_t mmax = 1;
+  bool easy = false;
+  int dsum = 0, S = 1, D = 1;
+#pragma unroll
+  for (int d = 3; d >= 0; --d) {
+    int bmax = -1, dfirst = 0;
+    bool nonunique = false, dvar = false;
+    for (int x = 0; x < c.cd[d]; ++x) {
+      const int olo = x * c.dpiece[d];
+      int lo, hi;
+      need_interval(c, d, olo, olo + c.dpiece[d], &lo, &hi);
+      const geo::DimStats<int> st = dim_stats_fast(lo, hi, c.spiece[d], c.rcp[d]);
+      const int delta = st.arg * S - x * D;
+      if (st.best > bmax) {
+        bmax = st.best, nonunique = !st.unique, dvar = false, dfirst = delta;
+      } else if (st.best == bmax) {
+        nonunique |= !st.unique;
+        dvar |= delta != dfirst;
+      }
+    }
+    mmax *= bmax;
+    easy |= nonunique | dvar;
+    dsum += dfirst;
+    S *= c.cs[d];
+    D *= c.cd[d];
+  }
+  if (mmax == 0) return 0;
+  if (easy || dsum != 0) return mmax;
+  return -1;
+}
+
+// The per-q walk (geometry.hpp: max_offdiag_volume) over destination
+// partitions q = q0, q0 + dq, ... — one lane's share of a warp-cooperative walk.
+__device__ __forceinline__ int64_t xfer_maxvol_walk(const XferCell &c, int q0, int dq) {
+  const int td = c.cd[0] * c.cd[1] * c.cd[2] * c.cd[3];
   int64_t maxvol = 0;
-  int changed = 0;
-  for (int q = 0; q < td; ++q) {
-    if (changed <= 3) {
-      int olo[4], ohi[4], lo[4], hi[4];
+  for (int q = q0; q < td; q += dq) {
+    int dig[4], r = q;
 #pragma unroll
-      for (int d = 0; d < 4; ++d) olo[d] = dig[d] * dpiece[d], ohi[d] = olo[d] + dpiece[d];
-      geo::required_box_owned<int, int>(kind, par, ss, band, olo, ohi, lo, hi);
+    for (int d = 3; d >= 0; --d) dig[d] = r % c.cd[d], r /= c.cd[d];
+    int olo[4], ohi[4], lo[4], hi[4];
 #pragma unroll
-      for (int d = 0; d < 4; ++d)
-        if (d >= changed) st[d] = dim_stats_fast(lo[d], hi[d], spiece[d], rcp[d]);
-    }
-    // combine (geometry.hpp: max_offdiag_volume)
+    for (int d = 0; d < 4; ++d) olo[d] = dig[d] * c.dpiece[d], ohi[d] = olo[d] + c.dpiece[d];
+    geo::required_box_owned<int, int>(c.kind, c.par, c.ss, c.band, olo, ohi, lo, hi);
+    geo::DimStats<int> st[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) st[d] = dim_stats_fast(lo[d], hi[d], c.spiece[d], c.rcp[d]);
     const int64_t M = static_cast<int64_t>(st[0].best) * st[1].best * st[2].best * st[3].best;
-    if (M > maxvol) {
-      const bool unique = st[0].unique && st[1].unique && st[2].unique && st[3].unique;
-      int64_t v = M;
-      if (unique && ((st[0].arg * cs[1] + st[1].arg) * cs[2] + st[2].arg) * cs[3] + st[3].arg == q) {
-        v = 0;
+    if (M <= maxvol) continue;
+    const bool unique = st[0].unique && st[1].unique && st[2].unique && st[3].unique;
+    int64_t v = M;
+    if (unique && ((st[0].arg * c.cs[1] + st[1].arg) * c.cs[2] + st[2].arg) * c.cs[3] + st[3].arg == q) {
+      v = 0;
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
-          int64_t x = st[d].second;
+      for (int d = 0; d < 4; ++d) {
+        int64_t x = st[d].second;
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (e != d) x *= st[e].best;
-          v = x > v ? x : v;
-        }
-      }
-      maxvol = v > maxvol ? v : maxvol;
-    }
-    // odometer over destination digits (W fastest), unrolled: constant indices
-    changed = 3;
-    if (++dig[3] == cd[3]) {
-      dig[3] = 0, changed = 2;
-      if (++dig[2] == cd[2]) {
-        dig[2] = 0, changed = 1;
-        if (++dig[1] == cd[1]) dig[1] = 0, changed = 0, ++dig[0];
+        for (int e = 0; e < 4; ++e)
+          if (e != d) x *= st[e].best;
+        v = x > v ? x : v;
       }
     }
+    maxvol = v > maxvol ? v : maxvol;
   }
   return maxvol;
 }
 
-__device__ inline void xfer_cell(const BuildArgs &a, const EdgeDev &E, int64_t cell) {
-  // cells are walked destination-config-major (consecutive threads share c_dst, so the
-  // q loop has the same trip count across a warp); the table stays row-major [i][j]
-  const int j = static_cast<int>(cell / E.nu), i = static_cast<int>(cell - static_cast<int64_t>(j) * E.nu);
-  const int64_t out = E.out_off + static_cast<int64_t>(i) * E.nv + j;
-  const int32_t *cs64 = a.cfg + 4 * (E.cat_u + i);
-  const int32_t *cd64 = a.cfg + 4 * (E.cat_v + j);
-  int cs[4], cd[4], ss[4], dpiece[4], spiece[4];
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    cs[d] = static_cast<int>(cs64[d]);
-    cd[d] = static_cast<int>(cd64[d]);
-    ss[d] = static_cast<int>(E.sshape[d]);
-    spiece[d] = ss[d] / cs[d];
-    dpiece[d] = static_cast<int>(E.dshape[d]) / cd[d];
-  }
-  const int td = cd[0] * cd[1] * cd[2] * cd[3];
-  const int band = static_cast<int>(E.band);
+__device__ __forceinline__ double xfer_seconds(const BuildArgs &a, int64_t maxvol) {
+  return maxvol > 0 ? 4.0 * static_cast<double>(maxvol) / a.bw_uniform : 0.0;
+}
+
+// Per-pair bandwidth: every (q, p) pair in reference order (cost.hpp:113-129).
+__device__ __forceinline__ double xfer_seconds_pairs(const BuildArgs &a, const XferCell &c) {
+  const int td = c.cd[0] * c.cd[1] * c.cd[2] * c.cd[3];
+  const int ts = c.cs[0] * c.cs[1] * c.cs[2] * c.cs[3];
   double seconds = 0.0;
-  if (a.bw_uniform > 0.0) {
-    const int64_t maxvol = xfer_maxvol_uniform(E, cs, cd, ss, spiece, dpiece, band);
-    if (maxvol > 0) seconds = 4.0 * static_cast<double>(maxvol) / a.bw_uniform;
-    a.xfer[out] = seconds;
-    return;
-  }
   int dig[4] = {0, 0, 0, 0};
-  int64_t maxvol = 0;
   for (int q = 0; q < td; ++q) {
     int olo[4], ohi[4], lo[4], hi[4];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) olo[d] = dig[d] * dpiece[d], ohi[d] = olo[d] + dpiece[d];
-    geo::required_box_owned<int, int64_t>(E.kind, E.params, ss, band, olo, ohi, lo, hi);
+    for (int d = 0; d < 4; ++d) olo[d] = dig[d] * c.dpiece[d], ohi[d] = olo[d] + c.dpiece[d];
+    geo::required_box_owned<int, int>(c.kind, c.par, c.ss, c.band, olo, ohi, lo, hi);
     if (geo::box_volume<int>(lo, hi) != 0) {
-      if (a.bw_uniform > 0.0) {
-        maxvol = geo::imax<int64_t>(maxvol, geo::max_offdiag_volume<int>(spiece, cs, lo, hi, q));
-      } else {
-        int pd[4] = {0, 0, 0, 0};
-        const int ts = cs[0] * cs[1] * cs[2] * cs[3];
-        for (int p = 0; p < ts; ++p) {
-          if (p != q) {
-            int64_t vol = 1;
+      int pd[4] = {0, 0, 0, 0};
+      for (int p = 0; p < ts; ++p) {
+        if (p != q) {
+          int64_t vol = 1;
 #pragma unroll
-            for (int d = 0; d < 4; ++d) {
-              const int plo = pd[d] * spiece[d];
-              vol *= geo::imax<int>(0, geo::imin<int>(plo + spiece[d], hi[d]) - geo::imax<int>(plo, lo[d]));
-            }
-            if (vol > 0) seconds = fmax(seconds, 4.0 * static_cast<double>(vol) / a.bw[static_cast<int64_t>(p) * a.D + q]);
+          for (int d = 0; d < 4; ++d) {
+            const int plo = pd[d] * c.spiece[d];
+            vol *= geo::imax<int>(0, geo::imin<int>(plo + c.spiece[d], hi[d]) - geo::imax<int>(plo, lo[d]));
           }
-          for (int d = 3; d >= 0; --d) { // odometer over source digits
-            if (++pd[d] < cs[d]) break;
-            pd[d] = 0;
-          }
+          if (vol > 0) seconds = fmax(seconds, 4.0 * static_cast<double>(vol) / a.bw[static_cast<int64_t>(p) * a.D + q]);
+        }
+        for (int d = 3; d >= 0; --d) { // odometer over source digits
+          if (++pd[d] < c.cs[d]) break;
+          pd[d] = 0;
         }
       }
     }
     for (int d = 3; d >= 0; --d) { // odometer over destination digits
-      if (++dig[d] < cd[d]) break;
+      if (++dig[d] < c.cd[d]) break;
       dig[d] = 0;
     }
   }
-  if (a.bw_uniform > 0.0 && maxvol > 0) seconds = 4.0 * static_cast<double>(maxvol) / a.bw_uniform;
-  a.xfer[out] = seconds;
+  return seconds;
+}
+
+// One K1 cell per lane.  `edge` < 0 marks an inactive lane.  All 32 lanes of
+// the warp must call this together: cells the separable bound cannot settle
+// are then walked by the whole warp, one cell at a time, lanes striding q.
+__device__ __forceinline__ void xfer_cells_warp(const BuildArgs &a, int edge, int64_t cell) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  bool hard = false;
+  if (edge >= 0) {
+    XferCell c;
+    xfer_decode(a, a.edges[edge], cell, c);
+    if (a.bw_uniform > 0.0) {
+      const int64_t mv = xfer_maxvol_separable(c);
+      if (mv >= 0)
+        a.xfer[c.out] = xfer_seconds(a, mv);
+      else
+        hard = true;
+    } else {
+      a.xfer[c.out] = xfer_seconds_pairs(a, c);
+    }
+  }
+  unsigned pending = __ballot_sync(kFull, hard);
+  while (pending) {
+    const int src = __ffs(pending) - 1;
+    pending &= pending - 1;
+    const int e = __shfl_sync(kFull, edge, src);
+    const int64_t cl = __shfl_sync(kFull, cell, src);
+    XferCell c;
+    xfer_decode(a, a.edges[e], cl, c);
+    int64_t mv = xfer_maxvol_walk(c, lane, 32);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t other = __shfl_xor_sync(kFull, mv, o);
+      mv = other > mv ? other : mv;
+    }
+    if (lane == src) a.xfer[c.out] = xfer_seconds(a, mv);
+  }
 }
 
 } // namespace pp

@@ -63,21 +63,27 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads) dp_fused_ker
   if (a.has_build) {
     const BuildArgs &B = a.build;
     const int64_t n = B.ncells + a.xcells;
-    for (int64_t g = static_cast<int64_t>(blockIdx.x) * kFusedThreads + threadIdx.x; g < n; g += stride) {
+    // block-uniform trip count: xfer_cells_warp needs whole warps
+    for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * kFusedThreads; g0 < n; g0 += stride) {
+      const int64_t g = g0 + threadIdx.x;
       if (g < B.ncells) {
         node_cost_cell(B, g);
-        continue;
       }
-      const int64_t x = g - B.ncells;
-      int lo = 0, hi = B.ne - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (B.edges[mid].out_off <= x)
-          lo = mid;
-        else
-          hi = mid - 1;
+      int edge = -1;
+      int64_t x = g - B.ncells;
+      if (g >= B.ncells && g < n) {
+        int lo = 0, hi = B.ne - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (B.edges[mid].out_off <= x)
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        edge = lo;
+        x -= B.edges[lo].out_off;
       }
-      xfer_cell(B, B.edges[lo], x - B.edges[lo].out_off);
+      xfer_cells_warp(B, edge, x);
     }
     grid.sync();
   }

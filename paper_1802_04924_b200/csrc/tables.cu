@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_tables_kernel(BuildArgs a
   }
   const EdgeDev &E = a.edges[lo];
   const int64_t cell = (eb - E.blk_begin) * kBuildThreads + threadIdx.x;
-  if (cell < E.cells) xfer_cell(a, E, cell);
+  xfer_cells_warp(a, cell < E.cells ? lo : -1, cell);
 }
 
 // Seeded synthetic tables (config-5 sweep at sizes the host generator cannot
