@@ -25,7 +25,18 @@ template <class T> struct FusedWave {
   const MergeDesc<T> *merges;
   int32_t nf, nm;
   int64_t ftiles, items;
+  int64_t rot; // items before this wave: block (b + rot) mod grid runs item b, so
+               // a small wave's blocks are idle in the previous wave and stage early
+  int32_t narrow; // run by the first cluster alone (cluster barrier to a narrow successor)
+  int32_t n_chains; // > 0: a chain segment (several waves), items = its row groups
+  const ChainDesc *chains;
+  const FoldDesc<T> *cfolds;
 };
+
+__device__ __forceinline__ int64_t first_item(int64_t rot) {
+  const int64_t g = gridDim.x;
+  return (static_cast<int64_t>(blockIdx.x) + g - rot % g) % g;
+}
 
 template <class T> struct FusedArgs {
   int32_t has_build;
@@ -42,6 +53,9 @@ template <class T> struct FusedArgs {
   int32_t nblk;
   FinishArgs fin;
   uint64_t *stamps; // optional: %globaltimer after each phase (profiling)
+  int32_t stage;    // stage each wave's first item before the preceding barrier
+  uint64_t *trace;  // optional: 8 stamps per wave from the block running item 0
+  int32_t nc;       // cluster size (narrow waves run on blocks [0, nc))
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -52,10 +66,36 @@ __device__ __forceinline__ uint64_t global_ns() {
 
 constexpr int kFusedThreads = 256;
 
+// Stages this block's first item of wave W: its descriptor and, for a panel
+// tile, the operands not in f.late (all of them when `ready` == kPanelAll).
+template <class T>
+__device__ __forceinline__ void stage_item(const FusedWave<T> &W, int ready, PanelSmem<T> &p, StagedItem<T> &st) {
+  __syncthreads(); // the block's last item of the finishing wave may still read p / st
+  const int64_t b = first_item(W.rot);
+  if (b >= W.items || W.n_chains) {
+    if (threadIdx.x == 0) st.b = -1;
+    return;
+  }
+  if (b < W.ftiles) {
+    const FoldDesc<T> f = W.folds[find_fold(W.folds, W.nf, b)];
+    int mask = 0;
+    if (panel_fold(f)) {
+      mask = (kPanelAll & ~f.late) | ready;
+      panel_load<T>(f, b - f.tile_begin, mask, p);
+    }
+    if (threadIdx.x == 0) st.f = f, st.mask = mask, st.b = b;
+  } else {
+    const MergeDesc<T> m = W.merges[find_merge(W.merges, W.nm, b - W.ftiles)];
+    if (threadIdx.x == 0) st.m = m, st.b = b;
+  }
+}
+
 template <class T> __global__ void __launch_bounds__(kFusedThreads) dp_fused_kernel(FusedArgs<T> a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ WaveSmem<T> sm;
+  // dynamic: max(WaveSmem, the largest chain item) bytes
+  extern __shared__ __align__(16) unsigned char fused_smem[];
+  WaveSmem<T> &sm = *reinterpret_cast<WaveSmem<T> *>(fused_smem);
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kFusedThreads;
   const bool stamp = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
   int ph = 0;
@@ -88,11 +128,47 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads) dp_fused_ker
     grid.sync();
   }
   if (stamp) a.stamps[ph++] = global_ns();
+  // this block's first item of each wave is staged one wave early: its
+  // descriptor, and everything but the operands the finishing wave writes,
+  // load before the barrier, off the critical path after it
+  __shared__ StagedItem<T> st;
+  FusedWave<T> W;
+  if (a.n_waves > 0) {
+    W = a.waves[0];
+    stage_item<T>(W, kPanelAll, sm.p, st);
+    __syncthreads();
+  }
   for (int w = 0; w < a.n_waves; ++w) {
-    const FusedWave<T> W = a.waves[w];
-    for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x)
-      wave_item<T>(W.folds, W.nf, W.ftiles, W.merges, W.nm, it, sm);
-    grid.sync();
+    const bool narrow = W.narrow;
+    const int64_t b0 = narrow ? static_cast<int64_t>(blockIdx.x) : first_item(W.rot);
+    const int64_t step = narrow ? a.nc : gridDim.x;
+    uint64_t *tr = a.trace && b0 == 0 ? a.trace + 16 * w : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = global_ns();
+    if (W.n_chains)
+      for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x) chain_item<T>(W.chains, W.n_chains, W.cfolds, it, fused_smem);
+    else if (!narrow || static_cast<int>(blockIdx.x) < a.nc)
+      for (int64_t it = b0; it < W.items; it += step)
+        wave_item<T>(W.folds, W.nf, W.ftiles, W.merges, W.nm, it, sm, narrow ? nullptr : &st, it == 0 ? tr : nullptr);
+    bool next_narrow = false;
+    if (w + 1 < a.n_waves) {
+      W = a.waves[w + 1];
+      next_narrow = W.narrow;
+      if (a.stage && !next_narrow)
+        stage_item<T>(W, 0, sm.p, st);
+      else {
+        __syncthreads();
+        if (threadIdx.x == 0) st.b = -1;
+      }
+    }
+    if (tr && threadIdx.x == 0) tr[3] = global_ns();
+    if (narrow && next_narrow) {
+      // both waves live in the first cluster: a cluster barrier (release /
+      // acquire at cluster scope) orders its writes; other clusters skip ahead
+      if (static_cast<int>(blockIdx.x) < a.nc) cg::this_cluster().sync();
+    } else {
+      grid.sync();
+    }
+    if (tr && threadIdx.x == 0) tr[4] = global_ns();
     if (stamp) a.stamps[ph++] = global_ns();
   }
   using A = typename Acc<T>::type;

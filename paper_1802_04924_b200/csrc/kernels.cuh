@@ -25,8 +25,21 @@ template <class T> struct FoldDesc {
   int32_t nu, nw, nv;
   int32_t tiles_k;    // tiles along nv
   int64_t tile_begin; // first global tile id of this fold
-  int32_t small;      // 1: 16x16 output tiles (one cell per thread) for waves too small to fill the GPU
+  int32_t small;      // tile mode: 0 32x32 chunked, 1 16x16 chunked, kPanel16/8/4 panel tiles (nw <= kPanel)
+  int32_t late;       // fused kernel: operands written by the previous wave (kPanelT1 | kPanelT2)
 };
+
+// Panel tiles: small-wave folds with nw <= kPanel stage the whole j range of
+// an R x R output tile in shared memory with one batch of loads (one memory
+// latency instead of one per 32-j chunk); 256 / R^2 thread groups split the j
+// range (R = 16, 8, 4: 1, 4, 16 groups), shortening the per-thread scan when
+// a wave has few tiles.  In the fused kernel the operands the previous wave
+// did not write (w always, t1/t2 unless `late`) are staged before the barrier
+// that ends that wave.
+constexpr int kPanel = 128;
+enum : int { kPanelW = 1, kPanelT1 = 2, kPanelT2 = 4, kPanelAll = 7 };
+enum : int { kPanel16 = 2, kPanel8 = 3, kPanel4 = 4 };
+__host__ __device__ constexpr int panel_side(int mode) { return mode == kPanel16 ? 16 : mode == kPanel8 ? 8 : 4; }
 
 constexpr int kSmallTile = 16;
 
@@ -42,29 +55,373 @@ constexpr int kFoldThreads = 256;
 constexpr int kMergeThreads = 256;
 constexpr int kMergePerBlock = kMergeThreads * 8;
 
-template <class T> struct WaveSmem {
+template <class T> struct TileSmem {
   T As[kTile][kTile + 1];
   T Bs[kTile][kTile];
 };
+template <class T> struct PanelSmem {
+  T W[kPanel];
+  T A[16 * (kPanel + 1)]; // w[j] + t1[i][j], R rows of stride kPanel + 1
+  T B[kPanel * 17];       // t2[j][k], nw rows of R, stride R + 1 (conflict-free column reads)
+};
+// Chain segments (fused kernel): a run of waves whose folds form chains
+// f1 -> f2 -> ... (f_{k+1}.t1 = f_k.out) with every t2 ready before the run.
+// Row r of f_{k+1}.out depends on row r of f_k.out alone (Eq. 2 folds t1 row
+// by row), so one block carries a few rows through the whole chain in shared
+// memory: one grid barrier per segment instead of one per wave.
+constexpr int kChainRows = 4;  // rows per item (max)
+constexpr int kChainMax = 128; // max nw / nv of a chain fold
+struct ChainDesc {
+  int32_t first, n;  // folds [first, first + n) of the segment's fold list
+  int32_t nu, rows;  // t1 rows, rows per item
+  int64_t item_begin;
+  int32_t buf;       // elements per staging buffer (w + padded t2 of any fold of the segment)
+  int32_t pad;
+};
+
+template <class T> union WaveSmem {
+  TileSmem<T> t;
+  PanelSmem<T> p;
+};
+
+// Shared memory of a chain item (dynamic, in elements of T unless noted):
+// A'[rows][kChainMax + 1] | cur[rows][kChainMax] | 2 x staging buffer
+// (w[nw] + t2[nw][nv + 1]) | the chain's fold descriptors.
+template <class T> __host__ __device__ constexpr size_t chain_smem_bytes(int rows, int buf, int max_len) {
+  return (static_cast<size_t>(rows) * (2 * kChainMax + 1) + 2 * static_cast<size_t>(buf)) * sizeof(T) + 16 +
+         static_cast<size_t>(max_len) * sizeof(FoldDesc<T>);
+}
+
+// A work item whose descriptor (and, for a panel tile, the operands the
+// previous wave does not write) was staged before the barrier that starts its
+// wave (fused kernel; lives in shared memory).
+template <class T> struct StagedItem {
+  FoldDesc<T> f;
+  MergeDesc<T> m;
+  int64_t b;    // work item, -1: none
+  int32_t mask; // panel operands already in shared memory
+  int32_t pad;
+};
+
+template <class T> __device__ __forceinline__ bool panel_fold(const FoldDesc<T> &f) {
+  return f.small >= kPanel16;
+}
+
+// Stages operands `mask` of output tile `tile` of f (an R x R panel tile) into
+// p.  Every global load is issued before the first shared-memory store, so
+// the panel costs one memory latency; A holds w[j] + t1[i][j] (the
+// reference's first addition), reading w from p.W when it was staged earlier.
+template <class T, int R>
+__device__ __forceinline__ void panel_load_r(const FoldDesc<T> &f, int64_t tile, int mask, PanelSmem<T> &p) {
+  constexpr int kIt = R * kPanel / kFoldThreads;
+  static_assert(kPanel <= kFoldThreads, "one w entry per thread");
+  const int i0 = static_cast<int>(tile / f.tiles_k) * R;
+  const int k0 = static_cast<int>(tile % f.tiles_k) * R;
+  const bool lw = mask & kPanelW, l1 = mask & kPanelT1, l2 = mask & kPanelT2;
+  const bool own_w = lw && static_cast<int>(threadIdx.x) < f.nw;
+  const T vw = own_w ? f.w[threadIdx.x] : T(0);
+  T v1[kIt], w1[kIt], v2[kIt];
+#pragma unroll
+  for (int q = 0; q < kIt; ++q) {
+    const int idx = threadIdx.x + q * kFoldThreads;
+    const int r = idx / kPanel, j = idx % kPanel;
+    const bool in1 = l1 && j < f.nw && i0 + r < f.nu;
+    v1[q] = in1 ? __ldcg(&f.t1[static_cast<int64_t>(i0 + r) * f.nw + j]) : T(0);
+    w1[q] = in1 && lw ? f.w[j] : T(0);
+    const int jj = idx / R, c = idx % R;
+    v2[q] = (l2 && jj < f.nw && k0 + c < f.nv) ? __ldcg(&f.t2[static_cast<int64_t>(jj) * f.nv + k0 + c]) : T(0);
+  }
+  if (own_w) p.W[threadIdx.x] = vw;
+#pragma unroll
+  for (int q = 0; q < kIt; ++q) {
+    const int idx = threadIdx.x + q * kFoldThreads;
+    const int r = idx / kPanel, j = idx % kPanel;
+    if (l1 && j < f.nw) p.A[r * (kPanel + 1) + j] = (lw ? w1[q] : p.W[j]) + v1[q];
+    if (l2) p.B[(idx / R) * (R + 1) + idx % R] = v2[q];
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void panel_load(const FoldDesc<T> &f, int64_t tile, int mask, PanelSmem<T> &p) {
+  if (f.small == kPanel16)
+    panel_load_r<T, 16>(f, tile, mask, p);
+  else if (f.small == kPanel8)
+    panel_load_r<T, 8>(f, tile, mask, p);
+  else
+    panel_load_r<T, 4>(f, tile, mask, p);
+}
+
+__device__ __forceinline__ uint64_t trace_ns() {
+#ifdef PP_TRACE_CLOCK // microbenchmarks: SM cycles instead of ns
+  return static_cast<uint64_t>(clock64());
+#else
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+#endif
+}
+
+// Scan keys: candidates are compared as int64 keys, branch-free, starting
+// from LLONG_MAX (above every key).  FP64 keys are order-preserving bit
+// maps; -0.0 shares +0.0's key since the two compare equal.  Tables never
+// hold NaN (rejected at upload; analytic costs are finite).
+template <class T> __device__ __forceinline__ long long scan_key(T x);
+template <> __device__ __forceinline__ long long scan_key<double>(double x) {
+  long long b = __double_as_longlong(x);
+  b = b == LLONG_MIN ? 0 : b;
+  return b ^ ((b >> 63) & LLONG_MAX);
+}
+template <> __device__ __forceinline__ long long scan_key<int32_t>(int32_t x) { return x; }
+
+// keep (k, j) if it precedes (bk, bj) in the reference's argmin order: lower
+// value, then lower j
+__device__ __forceinline__ void keep_min(long long k, int j, long long &bk, int &bj) {
+  const bool t = k < bk || (k == bk && j < bj);
+  bk = t ? k : bk;
+  bj = t ? j : bj;
+}
+
+// One R x R panel tile: thread t owns cell t / G and scans j = g, g + G, ...
+// (G = 256 / R^2 groups, g = t % G); every merge prefers the lower j on
+// equal values, which reproduces the reference's ascending strict-< scan.
+template <class T, int R>
+__device__ __forceinline__ void panel_tile_r(const FoldDesc<T> &f, int64_t tile, int staged, PanelSmem<T> &p,
+                                             uint64_t *tr) {
+  constexpr int kCells = R * R, kG = kFoldThreads / kCells, kRS = R + 1;
+  if (staged != kPanelAll) panel_load_r<T, R>(f, tile, kPanelAll & ~staged, p);
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[1] = trace_ns();
+  // the kG groups of a cell are adjacent lanes: a shuffle tree merges them
+  const int g = threadIdx.x % kG, cell = threadIdx.x / kG;
+  const int ty = cell / R, tx = cell % R;
+  const T *Ar = p.A + ty * (kPanel + 1);
+  const T *Bc = p.B + tx;
+  // two chains (alternate candidates), four candidates per step with every
+  // shared-memory read issued before the compares; within a chain strict <
+  // keeps the lowest j, as the reference's ascending scan does
+  long long k0 = LLONG_MAX, k1 = LLONG_MAX;
+  int j0 = INT_MAX, j1 = INT_MAX;
+  const int nw = f.nw;
+  int j = g;
+  for (; j + 3 * kG < nw; j += 4 * kG) {
+    T a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = Ar[j + u * kG], b[u] = Bc[(j + u * kG) * kRS];
+    long long c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = scan_key<T>(a[u] + b[u]);
+#pragma unroll
+    for (int u = 0; u < 4; u += 2) {
+      if (c[u] < k0) k0 = c[u], j0 = j + u * kG;
+      if (c[u + 1] < k1) k1 = c[u + 1], j1 = j + (u + 1) * kG;
+    }
+  }
+  for (; j < nw; j += kG) {
+    const long long c = scan_key<T>(Ar[j] + Bc[j * kRS]);
+    if (c < k0) k0 = c, j0 = j;
+  }
+  keep_min(k1, j1, k0, j0);
+  if (tr && threadIdx.x == 0) tr[5] = trace_ns();
+#pragma unroll
+  for (int o = kG / 2; o > 0; o >>= 1) {
+    const long long ok = __shfl_xor_sync(0xffffffffu, k0, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, j0, o);
+    keep_min(ok, oj, k0, j0);
+  }
+  const int i = static_cast<int>(tile / f.tiles_k) * R + ty;
+  const int k = static_cast<int>(tile % f.tiles_k) * R + tx;
+  if (tr && threadIdx.x == 0) tr[6] = trace_ns();
+  if (g == 0 && i < f.nu && k < f.nv) {
+    f.out[static_cast<int64_t>(i) * f.nv + k] = Ar[j0] + Bc[j0 * kRS]; // the winner's own sum (keeps -0.0)
+    f.am[static_cast<int64_t>(i) * f.nv + k] = static_cast<uint16_t>(j0);
+  }
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[2] = trace_ns();
+}
+
+template <class T>
+__device__ __forceinline__ void panel_tile(const FoldDesc<T> &f, int64_t tile, int staged, PanelSmem<T> &p,
+                                           uint64_t *tr = nullptr) {
+  if (f.small == kPanel16)
+    panel_tile_r<T, 16>(f, tile, staged, p, tr);
+  else if (f.small == kPanel8)
+    panel_tile_r<T, 8>(f, tile, staged, p, tr);
+  else
+    panel_tile_r<T, 4>(f, tile, staged, p, tr);
+}
+
+template <class T> __device__ __forceinline__ void cp_async(T *dst, const T *src) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte elements");
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Stages fold f's w and t2 (rows padded to nv + 1) into buf, asynchronously.
+template <class T> __device__ __forceinline__ void chain_stage(const FoldDesc<T> &f, T *buf) {
+  for (int j = threadIdx.x; j < f.nw; j += kFoldThreads) cp_async(buf + j, f.w + j);
+  T *t2s = buf + f.nw;
+  const int per = max(1, kFoldThreads / f.nv);
+  const int jr = threadIdx.x / f.nv, v = threadIdx.x - jr * f.nv;
+  if (jr < per)
+    for (int j = jr; j < f.nw; j += per) cp_async(t2s + j * (f.nv + 1) + v, f.t2 + static_cast<int64_t>(j) * f.nv + v);
+  cp_async_commit();
+}
+
+// Item `it` of a chain segment: rows [r0, r0 + rows) of one chain, through
+// all its folds.  Fold k + 1's w and t2 stream into shared memory (cp.async)
+// while fold k computes; its rows live in shared memory between folds.  Per
+// fold: A' = w + t1 rows (the reference's first addition), then threads =
+// (row, col) cells x G j-groups (adjacent lanes) scan j = g, g + G, ... and a
+// shuffle tree merges the groups (lower value, then lower j: the reference's
+// ascending strict-< scan).  Writes every fold's argmins and the last fold's
+// table; the intermediate tables have no other reader.
+template <class T>
+__device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains, const FoldDesc<T> *cf, int64_t it,
+                                           unsigned char *smem, uint64_t *tr = nullptr) {
+  const bool stamp = tr && threadIdx.x == 0;
+  int lo = 0, hi = n_chains - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (chains[mid].item_begin <= it)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const ChainDesc c = chains[lo];
+  const int r0 = static_cast<int>(it - c.item_begin) * c.rows;
+  const int nr = min(c.rows, c.nu - r0);
+  T *A = reinterpret_cast<T *>(smem);
+  T *cur = A + c.rows * (kChainMax + 1);
+  T *buf[2] = {cur + c.rows * kChainMax, cur + c.rows * kChainMax + c.buf};
+  FoldDesc<T> *fd = reinterpret_cast<FoldDesc<T> *>(
+      (reinterpret_cast<uintptr_t>(buf[1] + c.buf) + 15) & ~uintptr_t(15));
+  __syncthreads(); // the block's previous item may still read smem
+  for (int k = threadIdx.x; k < c.n; k += kFoldThreads) fd[k] = cf[c.first + k];
+  {
+    const FoldDesc<T> f0 = cf[c.first];
+    chain_stage<T>(f0, buf[0]);
+    for (int x = threadIdx.x; x < nr * f0.nw; x += kFoldThreads) {
+      const int r = x / f0.nw, j = x - r * f0.nw;
+      cur[r * kChainMax + j] = __ldcg(&f0.t1[static_cast<int64_t>(r0 + r) * f0.nw + j]);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < c.n; ++k) {
+    const FoldDesc<T> &f = fd[k];
+    const int nw = f.nw, nv = f.nv;
+    const T *bw = buf[k & 1], *t2s = bw + nw;
+    if (stamp && k < 4) tr[4 * k] = trace_ns();
+    if (k + 1 < c.n) {
+      chain_stage<T>(fd[k + 1], buf[(k + 1) & 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (stamp && k < 4) tr[4 * k + 1] = trace_ns();
+    for (int x = threadIdx.x; x < nr * nw; x += kFoldThreads) {
+      const int r = x / nw, j = x - r * nw;
+      A[r * (kChainMax + 1) + j] = bw[j] + cur[r * kChainMax + j];
+    }
+    __syncthreads();
+    if (stamp && k < 4) tr[4 * k + 2] = trace_ns();
+    const int cells = nr * nv;
+    int G = 1;
+    while (G < 32 && cells * G * 2 <= kFoldThreads) G *= 2;
+    const int g = threadIdx.x % G, slots = kFoldThreads / G;
+    const bool last = k + 1 == c.n;
+    for (int cell = threadIdx.x / G; cell < (cells + slots - 1) / slots * slots; cell += slots) {
+      const bool live = cell < cells;
+      const int r = live ? cell / nv : 0, v = live ? cell - r * nv : 0;
+      const T *a = A + r * (kChainMax + 1);
+      const T *t = t2s + v;
+      long long k0 = LLONG_MAX, k1 = LLONG_MAX;
+      int j0 = INT_MAX, j1 = INT_MAX;
+      if (live) {
+        int j = g;
+        for (; j + 3 * G < nw; j += 4 * G) {
+          long long cc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cc[u] = scan_key<T>(a[j + u * G] + t[(j + u * G) * (nv + 1)]);
+#pragma unroll
+          for (int u = 0; u < 4; u += 2) {
+            if (cc[u] < k0) k0 = cc[u], j0 = j + u * G;
+            if (cc[u + 1] < k1) k1 = cc[u + 1], j1 = j + (u + 1) * G;
+          }
+        }
+        for (; j < nw; j += G) {
+          const long long c0 = scan_key<T>(a[j] + t[j * (nv + 1)]);
+          if (c0 < k0) k0 = c0, j0 = j;
+        }
+        keep_min(k1, j1, k0, j0);
+      }
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const long long ok = __shfl_xor_sync(0xffffffffu, k0, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, j0, o);
+        keep_min(ok, oj, k0, j0);
+      }
+      if (live && g == 0) {
+        const T val = a[j0] + t[j0 * (nv + 1)];
+        const int64_t o = static_cast<int64_t>(r0 + r) * nv + v;
+        f.am[o] = static_cast<uint16_t>(j0);
+        if (last)
+          f.out[o] = val;
+        else
+          cur[r * kChainMax + v] = val;
+      }
+    }
+    __syncthreads();
+    if (stamp && k < 4) tr[4 * k + 3] = trace_ns();
+  }
+}
+
+template <class T> __device__ __forceinline__ int find_fold(const FoldDesc<T> *folds, int n_folds, int64_t b) {
+  int lo = 0, hi = n_folds - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (folds[mid].tile_begin <= b)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+template <class T> __device__ __forceinline__ int find_merge(const MergeDesc<T> *merges, int n_merges, int64_t mb) {
+  int lo = 0, hi = n_merges - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (merges[mid].blk_begin <= mb)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
 
 // Work item b of a wave: b < fold_tiles folds one 32x32 output tile of a fold
 // (block-cooperative, uses `sm`); otherwise it adds one merge chunk.
 template <class T>
 __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds, int64_t fold_tiles,
-                                          const MergeDesc<T> *merges, int n_merges, int64_t b, WaveSmem<T> &sm) {
-  auto &As = sm.As;
-  auto &Bs = sm.Bs;
+                                          const MergeDesc<T> *merges, int n_merges, int64_t b, WaveSmem<T> &sm,
+                                          const StagedItem<T> *pre = nullptr, uint64_t *tr = nullptr) {
+  auto &As = sm.t.As;
+  auto &Bs = sm.t.Bs;
+  const bool staged = pre && pre->b == b;
   if (b < fold_tiles) {
-    int lo = 0, hi = n_folds - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (folds[mid].tile_begin <= b)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    const FoldDesc<T> f = folds[lo];
+    const FoldDesc<T> f = staged ? pre->f : folds[find_fold(folds, n_folds, b)];
     const int64_t tile = b - f.tile_begin;
+    if (panel_fold(f)) {
+      panel_tile<T>(f, tile, staged ? pre->mask : 0, sm.p, tr);
+      return;
+    }
     if (f.small) { // 16x16 tile, one cell per thread, two interleaved scans
       const int i0 = static_cast<int>(tile / f.tiles_k) * kSmallTile;
       const int k0 = static_cast<int>(tile % f.tiles_k) * kSmallTile;
@@ -78,10 +435,10 @@ __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds,
           const int idx = threadIdx.x + q * kFoldThreads;
           const int r = idx >> 5, c = idx & 31; // A: 16 rows x 32 j
           const int i = i0 + r, j = j0 + c;
-          pa[q] = (i < f.nu && j < f.nw) ? T(f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j]) : T(0);
+          pa[q] = (i < f.nu && j < f.nw) ? T(f.w[j] + __ldcg(&f.t1[static_cast<int64_t>(i) * f.nw + j])) : T(0);
           const int jr = idx >> 4, kc = idx & 15; // B: 32 j x 16 cols
           const int jj = j0 + jr, k = k0 + kc;
-          pb[q] = (jj < f.nw && k < f.nv) ? f.t2[static_cast<int64_t>(jj) * f.nv + k] : T(0);
+          pb[q] = (jj < f.nw && k < f.nv) ? __ldcg(&f.t2[static_cast<int64_t>(jj) * f.nv + k]) : T(0);
         }
       };
       fetch(0);
@@ -135,9 +492,9 @@ __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds,
       for (int q = 0; q < 4; ++q) {
         const int idx = threadIdx.x + q * kFoldThreads, r = idx >> 5, c = idx & 31;
         const int i = i0 + r, j = j0 + c;
-        pa[q] = (i < f.nu && j < f.nw) ? T(f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j]) : T(0);
+        pa[q] = (i < f.nu && j < f.nw) ? T(f.w[j] + __ldcg(&f.t1[static_cast<int64_t>(i) * f.nw + j])) : T(0);
         const int jj = j0 + r, k = k0 + c;
-        pb[q] = (jj < f.nw && k < f.nv) ? f.t2[static_cast<int64_t>(jj) * f.nv + k] : T(0);
+        pb[q] = (jj < f.nw && k < f.nv) ? __ldcg(&f.t2[static_cast<int64_t>(jj) * f.nv + k]) : T(0);
       }
     };
     fetch(0);
@@ -188,18 +545,10 @@ __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds,
     return;
   }
   const int64_t mb = b - fold_tiles;
-  int lo = 0, hi = n_merges - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (merges[mid].blk_begin <= mb)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  const MergeDesc<T> m = merges[lo];
+  const MergeDesc<T> m = staged ? pre->m : merges[find_merge(merges, n_merges, mb)];
   const int64_t base = (mb - m.blk_begin) * kMergePerBlock;
   for (int64_t k = base + threadIdx.x; k < m.n && k < base + kMergePerBlock; k += kMergeThreads)
-    m.out[k] = m.a[k] + m.b[k];
+    m.out[k] = __ldcg(&m.a[k]) + __ldcg(&m.b[k]);
 }
 
 // One launch per wave: blocks [0, fold_tiles) fold 32x32 output tiles, the

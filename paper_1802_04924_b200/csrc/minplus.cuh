@@ -28,6 +28,8 @@
 //   mp_rescan  first j of the winning chunk; out = ra + cb + best, am = j
 #pragma once
 
+#include "kernels.cuh"
+
 #include <climits>
 #include <cstdint>
 
@@ -157,8 +159,7 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// cp_async_commit / cp_async_wait: kernels.cuh
 
 __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *folds, int n) {
   extern __shared__ __align__(16) unsigned char mp_smem[];

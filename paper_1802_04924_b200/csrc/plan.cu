@@ -24,6 +24,14 @@
 #include <map>
 
 namespace pp {
+// tuning knobs read per prepare (A/B experiments in one process)
+static int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+}
+
+namespace pp {
 
 namespace {
 
@@ -88,6 +96,8 @@ struct pp_prepared {
   bool launched = false, uploaded = false;
   size_t stamp_off = 0; // fused kernel phase stamps (image offset), n_stamps entries
   int n_stamps = 0;
+  size_t trace_off = 0; // PARPLAN_WAVE_TRACE: 8 stamps per wave (printed by pp_plan_profile)
+  std::vector<char> phase_chain; // fused phases that are chain segments (profile kind 16)
   std::vector<double> fused_wave_work;
 
   ~pp_prepared() {
@@ -153,12 +163,14 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   std::vector<size_t> tab_off(static_cast<size_t>(E_total), 0), am_off(s.ops.size(), 0);
   std::vector<size_t> amfull_off(s.ops.size(), 0), gat_off(static_cast<size_t>(E_total), SIZE_MAX);
   size_t am_bytes = 0, amfull_bytes = 0, gat_bytes = 0;
+  std::vector<int> prod_wave(static_cast<size_t>(E_total), 0); // wave writing each table (0: original)
   for (int w = 1; w <= s.n_waves; ++w) {
     const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
     for (int x = x0; x < x1; ++x) {
       const int oi = s.exec[static_cast<size_t>(x)];
       const Op &op = s.ops[static_cast<size_t>(oi)];
       tab_off[static_cast<size_t>(op.ne)] = tab_plan.alloc(store_cells(op.ne) * sizeof(T));
+      prod_wave[static_cast<size_t>(op.ne)] = w;
       if (!op.type) {
         am_off[static_cast<size_t>(oi)] = am_bytes;
         am_bytes += align256(store_cells(op.ne) * 2);
@@ -306,10 +318,21 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<WaveRange> waves;
     std::vector<std::tuple<const void *, void *, size_t>> final_gathers; // sharded: final edges + argmins
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
-    size_t oG, oT, oFW, oST;
+    size_t oG, oT, oFW, oST, oTR;
+    int n_phases = 0;                // fused kernel: waves / chain segments
+    size_t dyn_smem = 0;             // fused kernel dynamic shared memory
+    std::vector<char> phase_chain;   // phase is a chain segment
+    std::vector<double> phase_work;  // cells per fused phase
     int nG;
     size_t res_bytes;
   };
+  const bool use_fused = mp_bytes == 0 && !ctx->no_fused && !shard;
+  // fused kernel: waves with at most kNarrowItems work items run on the first
+  // thread-block cluster alone, with cluster barriers between consecutive
+  // narrow waves instead of grid-wide ones
+  const int fused_nc = use_fused ? std::max(1, env_int("PARPLAN_CLUSTER", 1)) : 1;
+  const int64_t narrow_items = use_fused ? env_int("PARPLAN_NARROW_ITEMS", 0) : 0;
+  const size_t kChainSmemMax = static_cast<size_t>(env_int("PARPLAN_CHAIN_SMEM_KB", 110)) * 1024;
   auto make_image = [&](unsigned char *db) {
     Image im;
     auto tabp = [&](int id) -> const T * {
@@ -332,6 +355,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     auto t2p = [&](int id) -> const T * { return shard && id >= t.ne ? gatp(id) : tabp(id); };
     auto amp = [&](int oi) { return reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]); };
     std::vector<FoldDesc<T>> folds;
+    struct FoldOps {
+      int e1, e2, ne, wave;
+    };
+    std::vector<FoldOps> fold_ops;
     std::vector<MergeDesc<T>> merges;
     std::vector<MpFold> mpf;
     for (int w = 1; w <= s.n_waves; ++w) {
@@ -347,7 +374,25 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
                      ((cols[static_cast<size_t>(op.e2)] + kTile - 1) / kTile);
       }
       const bool small_wave = big_tiles < 2 * int64_t(ctx->sms);
-      const int ts = small_wave ? kSmallTile : kTile;
+      // panel tiles: the smallest side whose tile count still fits one round
+      // of co-resident blocks (more j-split groups, shorter scans)
+      int panel_mode = kPanel16;
+      if (small_wave && env_int("PARPLAN_PANEL", 1)) {
+        const int forced = env_int("PARPLAN_PANEL_SIDE", 0);
+        for (int mode : {kPanel4, kPanel8}) {
+          const int R = panel_side(mode);
+          int64_t n = 0;
+          for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+            const Op &op = s.ops[static_cast<size_t>(s.exec[static_cast<size_t>(x)])];
+            if (op.type || large[static_cast<size_t>(s.exec[static_cast<size_t>(x)])]) continue;
+            n += static_cast<int64_t>((nu_eff(op.e1) + R - 1) / R) * ((cols[static_cast<size_t>(op.e2)] + R - 1) / R);
+          }
+          if (forced ? R == forced : n <= 2 * int64_t(ctx->sms)) {
+            panel_mode = mode;
+            break;
+          }
+        }
+      }
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
@@ -406,7 +451,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           f.nu = nu_eff(op.e1);
           f.nw = t.counts[static_cast<size_t>(op.removed)];
           f.nv = cols[static_cast<size_t>(op.e2)];
-          f.small = small_wave ? 1 : 0;
+          f.small = small_wave ? (f.nw <= kPanel && env_int("PARPLAN_PANEL", 1) ? panel_mode : 1) : 0;
+          const int ts = f.small >= kPanel16 ? panel_side(f.small) : f.small ? kSmallTile : kTile;
+          f.late = 0; // set below, once the narrow waves are known
+          fold_ops.push_back({op.e1, op.e2, op.ne, w});
           f.tiles_k = (f.nv + ts - 1) / ts;
           f.tile_begin = wr.ftiles;
           wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
@@ -427,6 +475,102 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         }
       }
       im.waves.push_back(wr);
+    }
+    // fused kernel: which waves run on the first cluster alone, and which
+    // operands of a wave's first item may be staged during the previous wave:
+    // those every block has seen through a grid barrier that ended a wave
+    // x <= w - 2 (a narrow-to-narrow step ends in a cluster barrier only)
+    const int nwv = s.n_waves;
+    // chain segments (fused kernel, chain_item): maximal runs of >= 2 waves of
+    // folds only, each fold's t2 written before the run and its t1 before the
+    // run or by a fold of the run (whose chain it extends)
+    struct Segment {
+      int ws, we; // waves [ws, we]
+      std::vector<ChainDesc> chains;
+      std::vector<FoldDesc<T>> cf;
+      int64_t items;
+      size_t smem = 0; // dynamic shared memory of its items
+    };
+    std::vector<Segment> segs;
+    std::vector<int> seg_of(static_cast<size_t>(nwv) + 2, -1);
+    if (use_fused && env_int("PARPLAN_CHAINS", 1)) {
+      auto fits = [&](int w, int ws) {
+        const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
+        if (wr.nm || wr.nf == 0) return false;
+        for (size_t q = wr.f0; q < wr.f0 + static_cast<size_t>(wr.nf); ++q) {
+          const FoldOps &o = fold_ops[q];
+          if (folds[q].nw > kChainMax || folds[q].nv > kChainMax) return false;
+          if (chain_smem_bytes<T>(1, folds[q].nw * (folds[q].nv + 2), 64) > kChainSmemMax) return false;
+          if (prod_wave[static_cast<size_t>(o.e2)] >= ws) return false;
+          const int p1 = prod_wave[static_cast<size_t>(o.e1)];
+          if (p1 >= ws && p1 >= w) return false;
+        }
+        return true;
+      };
+      for (int w = 1; w <= nwv;) {
+        int we = w;
+        if (fits(w, w))
+          while (we + 1 <= nwv && fits(we + 1, w)) ++we;
+        if (we > w) {
+          Segment sg{w, we, {}, {}, 0, 0};
+          std::vector<int> chain_of_table(static_cast<size_t>(E_total), -1);
+          std::vector<std::vector<size_t>> members;
+          for (int x = w; x <= we; ++x) {
+            const WaveRange &wr = im.waves[static_cast<size_t>(x) - 1];
+            for (size_t q = wr.f0; q < wr.f0 + static_cast<size_t>(wr.nf); ++q) {
+              const FoldOps &o = fold_ops[q];
+              int c = prod_wave[static_cast<size_t>(o.e1)] >= w ? chain_of_table[static_cast<size_t>(o.e1)] : -1;
+              if (c < 0) {
+                c = static_cast<int>(members.size());
+                members.emplace_back();
+              }
+              members[static_cast<size_t>(c)].push_back(q);
+              chain_of_table[static_cast<size_t>(o.ne)] = c;
+            }
+          }
+          int64_t rows_total = 0;
+          int buf = 0, max_len = 0;
+          for (const auto &m : members) {
+            rows_total += folds[m.front()].nu;
+            max_len = std::max(max_len, static_cast<int>(m.size()));
+            for (size_t q : m) buf = std::max(buf, folds[q].nw * (folds[q].nv + 2));
+          }
+          buf = (buf + 3) & ~3; // keeps the second buffer 16-byte aligned
+          const int64_t cap = 2 * int64_t(ctx->sms);
+          int rows = static_cast<int>(std::clamp<int64_t>((rows_total + cap - 1) / cap, 1, kChainRows));
+          while (rows > 1 && chain_smem_bytes<T>(rows, buf, max_len) > kChainSmemMax) --rows;
+          sg.smem = chain_smem_bytes<T>(rows, buf, max_len);
+          for (const auto &m : members) {
+            ChainDesc cd{static_cast<int32_t>(sg.cf.size()), static_cast<int32_t>(m.size()), folds[m.front()].nu, rows,
+                         sg.items, buf, 0};
+            for (size_t q : m) sg.cf.push_back(folds[q]);
+            sg.items += (cd.nu + rows - 1) / rows;
+            sg.chains.push_back(cd);
+          }
+          for (int x = w; x <= we; ++x) seg_of[static_cast<size_t>(x)] = static_cast<int>(segs.size());
+          segs.push_back(std::move(sg));
+        }
+        w = we + 1;
+      }
+    }
+    std::vector<char> narrow(static_cast<size_t>(nwv) + 2, 0), gbar(static_cast<size_t>(nwv) + 2, 1);
+    for (int w = 1; w <= nwv; ++w) {
+      const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
+      narrow[static_cast<size_t>(w)] = seg_of[static_cast<size_t>(w)] < 0 && wr.ftiles + wr.mblocks <= narrow_items;
+    }
+    for (int w = 1; w < nwv; ++w) // inside a segment no barrier separates the waves
+      if (seg_of[static_cast<size_t>(w)] >= 0 && seg_of[static_cast<size_t>(w)] == seg_of[static_cast<size_t>(w) + 1])
+        gbar[static_cast<size_t>(w)] = 0;
+    for (int w = 1; w < nwv; ++w)
+      if (narrow[static_cast<size_t>(w)] && narrow[static_cast<size_t>(w) + 1]) gbar[static_cast<size_t>(w)] = 0;
+    std::vector<int> seen(static_cast<size_t>(nwv) + 2, 0); // data of waves <= seen[w] is visible while wave w - 1 runs
+    for (int w = 3; w <= nwv; ++w)
+      seen[static_cast<size_t>(w)] = gbar[static_cast<size_t>(w) - 2] ? w - 2 : seen[static_cast<size_t>(w) - 1];
+    for (size_t q = 0; q < folds.size(); ++q) {
+      const FoldOps &o = fold_ops[q];
+      const int vis = seen[static_cast<size_t>(o.wave)];
+      folds[q].late = (prod_wave[static_cast<size_t>(o.e1)] > vis ? kPanelT1 : 0) |
+                      (prod_wave[static_cast<size_t>(o.e2)] > vis || (shard && o.e2 >= t.ne) ? kPanelT2 : 0);
     }
     std::vector<EnumNode> en(static_cast<size_t>(K));
     for (int d = 0; d < K; ++d) {
@@ -469,14 +613,48 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     im.oMP = pk.put(mpf);
     im.oF = pk.put(folds);
     im.oM = pk.put(merges);
-    { // per-wave work lists of the fused kernel (pointers into the sections above)
+    { // per-phase work lists of the fused kernel (pointers into the sections above):
+      // one entry per wave, or per chain segment
       std::vector<FusedWave<T>> fw;
-      for (const auto &wr : im.waves)
-        fw.push_back(FusedWave<T>{reinterpret_cast<const FoldDesc<T> *>(db + off_image + im.oF) + wr.f0,
-                                  reinterpret_cast<const MergeDesc<T> *>(db + off_image + im.oM) + wr.m0, wr.nf, wr.nm,
-                                  wr.ftiles, wr.ftiles + wr.mblocks});
+      im.phase_work.clear();
+      int64_t rot = 0;
+      for (int w = 1; w <= nwv;) {
+        const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
+        const int sg = seg_of[static_cast<size_t>(w)];
+        if (sg >= 0) {
+          const Segment &S = segs[static_cast<size_t>(sg)];
+          const size_t oc = pk.put(S.chains), of = pk.put(S.cf);
+          FusedWave<T> e{};
+          e.items = S.items;
+          e.n_chains = static_cast<int32_t>(S.chains.size());
+          e.chains = reinterpret_cast<const ChainDesc *>(db + off_image + oc);
+          e.cfolds = reinterpret_cast<const FoldDesc<T> *>(db + off_image + of);
+          fw.push_back(e);
+          double cells = 0.0;
+          for (int x = S.ws; x <= S.we; ++x) cells += im.waves[static_cast<size_t>(x) - 1].cells;
+          im.phase_work.push_back(cells);
+          w = S.we + 1;
+          continue;
+        }
+        const int64_t items = wr.ftiles + wr.mblocks;
+        FusedWave<T> e{};
+        e.folds = reinterpret_cast<const FoldDesc<T> *>(db + off_image + im.oF) + wr.f0;
+        e.merges = reinterpret_cast<const MergeDesc<T> *>(db + off_image + im.oM) + wr.m0;
+        e.nf = wr.nf, e.nm = wr.nm, e.ftiles = wr.ftiles, e.items = items, e.rot = rot;
+        e.narrow = narrow[static_cast<size_t>(w)];
+        fw.push_back(e);
+        im.phase_work.push_back(wr.cells);
+        if (env_int("PARPLAN_ROTATE", 1)) rot += items;
+        ++w;
+      }
       im.oFW = pk.put(fw);
-      im.oST = pk.put(std::vector<uint64_t>(im.waves.size() + 4));
+      im.n_phases = static_cast<int>(fw.size());
+      im.dyn_smem = sizeof(WaveSmem<T>);
+      for (const Segment &S : segs) im.dyn_smem = std::max(im.dyn_smem, S.smem);
+      im.phase_chain.clear();
+      for (const auto &e : fw) im.phase_chain.push_back(e.n_chains > 0);
+      im.oST = pk.put(std::vector<uint64_t>(fw.size() + 4));
+      im.oTR = env_int("PARPLAN_WAVE_TRACE", 0) ? pk.put(std::vector<uint64_t>(16 * fw.size())) : 0;
     }
     im.oN = pk.put(en);
     im.oE = pk.put(ee);
@@ -550,7 +728,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->step_work.clear();
   int launches = 0;
   // one cooperative kernel for the whole plan when no fold needs the S16x2 path
-  const bool use_fused = mp_bytes == 0 && !ctx->no_fused && !shard;
+  // (use_fused / fused_nc are decided before the image is built)
   auto push_gathers = [&](const std::vector<std::tuple<const void *, void *, size_t>> &list) {
     for (size_t g0 = 0; g0 < list.size(); g0 += 256) { // NCCL groups of <= 256 all-gathers
       std::vector<std::tuple<const void *, void *, size_t>> part(list.begin() + static_cast<long>(g0),
@@ -703,37 +881,71 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       fz.build = ba;
       fz.xcells = bp ? t.xcells : 0;
       fz.waves = reinterpret_cast<const FusedWave<T> *>(dimg + im.oFW);
-      fz.n_waves = static_cast<int32_t>(im.waves.size());
+      fz.n_waves = static_cast<int32_t>(im.n_phases);
       fz.en = en, fz.ee = ee, fz.k = K, fz.m = m;
       fz.space = space, fz.per_thread = per_thread;
       fz.blk_val = bv, fz.blk_idx = bi, fz.nblk = nblk;
       fz.fin = fa;
       fz.stamps = reinterpret_cast<uint64_t *>(dimg + im.oST);
+      fz.stage = env_int("PARPLAN_STAGE", 1);
+      fz.trace = im.oTR ? reinterpret_cast<uint64_t *>(dimg + im.oTR) : nullptr;
+      P->trace_off = im.oTR;
       P->stamp_off = im.oST;
-      P->n_stamps = static_cast<int>(im.waves.size()) + 4; // start, tables, waves..., enum, finish
-      P->fused_wave_work.clear();
-      for (const auto &wr : im.waves) P->fused_wave_work.push_back(wr.cells);
+      P->n_stamps = im.n_phases + 4; // start, tables, waves / segments..., enum, finish
+      P->fused_wave_work = im.phase_work;
+      P->phase_chain = im.phase_chain;
+      const size_t dyn = im.dyn_smem;
+      {
+        static size_t dyn_set[2] = {0, 0};
+        if (dyn_set[sizeof(T) == 8] < dyn) {
+          PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+          dyn_set[sizeof(T) == 8] = dyn;
+        }
+      }
       int occ = 0;
-      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_fused_kernel<T>, kFusedThreads, 0));
+      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_fused_kernel<T>, kFusedThreads, dyn));
       PP_REQUIRE(occ > 0, "fused plan kernel does not fit on an SM");
       int64_t items = std::max<int64_t>(nblk, 1);
       if (bp) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
       for (const auto &wr : im.waves) items = std::max<int64_t>(items, wr.ftiles + wr.mblocks);
-      static const int per_sm_env = std::getenv("PARPLAN_FUSED_BLOCKS_PER_SM")
-                                        ? std::atoi(std::getenv("PARPLAN_FUSED_BLOCKS_PER_SM"))
-                                        : 0;
+      const int per_sm_env = env_int("PARPLAN_FUSED_BLOCKS_PER_SM", 0);
       const int per_sm = per_sm_env > 0 ? std::min(per_sm_env, occ) : occ;
-      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, int64_t(ctx->sms) * per_sm));
-      P->steps.push_back([ctx, fz, grid](cudaStream_t st) {
+      // cooperative + cluster launch: the grid is whole clusters, all co-resident
+      const int nc = fused_nc;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = static_cast<unsigned>(nc), attr[1].val.clusterDim.y = 1, attr[1].val.clusterDim.z = 1;
+      int64_t cap = int64_t(ctx->sms) * per_sm;
+      if (nc > 1) {
+        static bool attr_set[2] = {false, false};
+        if (!attr_set[sizeof(T) == 8]) {
+          PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          attr_set[sizeof(T) == 8] = true;
+        }
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(static_cast<unsigned>(nc));
+        q.blockDim = dim3(kFusedThreads);
+        q.attrs = attr;
+        q.numAttrs = 2;
+        q.dynamicSmemBytes = dyn;
+        int clusters = 0;
+        PP_CUDA(cudaOccupancyMaxActiveClusters(&clusters, dp_fused_kernel<T>, &q));
+        PP_REQUIRE(clusters > 0, "fused plan kernel: no co-resident cluster of " + std::to_string(nc));
+        cap = std::min<int64_t>(cap, int64_t(clusters) * nc) / nc * nc;
+      }
+      const int64_t want = (items + nc - 1) / nc * nc;
+      const unsigned grid = static_cast<unsigned>(std::max<int64_t>(nc, std::min<int64_t>(want, cap)));
+      fz.nc = nc;
+      P->steps.push_back([ctx, fz, grid, attr, dyn, nc](cudaStream_t st) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kFusedThreads);
+        cfg.dynamicSmemBytes = dyn;
         cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.attrs = const_cast<cudaLaunchAttribute *>(attr);
+        cfg.numAttrs = nc > 1 ? 2 : 1;
         PP_CUDA(cudaLaunchKernelEx(&cfg, dp_fused_kernel<T>, fz));
         check_launch(ctx);
       });
@@ -928,12 +1140,28 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
         std::vector<uint64_t> st(static_cast<size_t>(P->n_stamps));
         PP_CUDA(cudaMemcpy(st.data(), P->dbase + P->image_off + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
         const int waves = P->n_stamps - 4;
+        if (P->trace_off) {
+          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves));
+          PP_CUDA(cudaMemcpy(tr.data(), P->dbase + P->image_off + P->trace_off, tr.size() * 8, cudaMemcpyDeviceToHost));
+          for (int w = 0; w < waves; ++w) {
+            const uint64_t *r = &tr[static_cast<size_t>(16 * w)];
+            const uint64_t b0 = st[static_cast<size_t>(w) + 1]; // block 0 left the previous barrier
+            auto rel = [&](uint64_t x) { return x ? static_cast<double>(static_cast<int64_t>(x - b0)) : -1.0; };
+            std::fprintf(stderr,
+                         "wave %2d worker start %6.0f tile %6.0f loaded %6.0f scanned %6.0f merged %6.0f stored %6.0f "
+                         "arrive %6.0f leave %6.0f ns\n",
+                         w, rel(r[0]), rel(r[7]), rel(r[1]), rel(r[5]), rel(r[6]), rel(r[2]), rel(r[3]), rel(r[4]));
+          }
+        }
         for (int ph = 0; ph + 1 < P->n_stamps; ++ph) {
-          const int pk = ph == 0 ? 11 : ph <= waves ? 12 : ph == waves + 1 ? 13 : 14;
+          const int pk = ph == 0       ? 11
+                         : ph <= waves ? (P->phase_chain[static_cast<size_t>(ph) - 1] ? 16 : 12)
+                         : ph == waves + 1 ? 13
+                                           : 14;
           kind_v.push_back(pk);
           ms_v.push_back(static_cast<double>(st[static_cast<size_t>(ph) + 1] - st[static_cast<size_t>(ph)]) * 1e-6);
           work_v.push_back(pk == 11 ? P->step_work[static_cast<size_t>(k)]
-                                    : pk == 12 ? P->fused_wave_work[static_cast<size_t>(ph - 1)] : 0.0);
+                                    : pk == 12 || pk == 16 ? P->fused_wave_work[static_cast<size_t>(ph - 1)] : 0.0);
         }
         kind_v.push_back(10); // launch + residual (kernel time not covered by phases)
         double covered = 0.0;

@@ -111,8 +111,10 @@ def test_prepared_plan_and_profile(gpu):
         assert list(r.indices) == list(want.indices) and r.cost == want.cost
     prof = prep.profile()
     kinds = [k for k, _, _ in prof]
-    assert kinds[0] == "fused.tables" and kinds.count("fused.wave") == r.waves and kinds[-1] == "fused"
-    assert sum(w for k, _, w in prof if k == "fused.wave") > 0
+    # one phase per wave, except chain segments (several waves, one phase)
+    phases = kinds.count("fused.wave") + kinds.count("fused.chain")
+    assert kinds[0] == "fused.tables" and 1 <= phases <= r.waves and kinds[-1] == "fused"
+    assert sum(w for k, _, w in prof if k in ("fused.wave", "fused.chain")) > 0
 
 
 def test_library_generators_match_reference_draw_order(gpu):
