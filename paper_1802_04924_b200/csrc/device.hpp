@@ -40,7 +40,9 @@ template <class T> struct DBuf {
   void alloc(size_t count) {
     release();
     own = true;
-    if (count) PP_CUDA(cudaMalloc(reinterpret_cast<void **>(&p), count * sizeof(T)));
+    // whole 256-byte granules: 16-byte-rounded bulk copies of a table's byte
+    // range (chain_item) stay inside the allocation
+    if (count) PP_CUDA(cudaMalloc(reinterpret_cast<void **>(&p), (count * sizeof(T) + 255) / 256 * 256));
     n = count;
   }
   void ensure(size_t count) {

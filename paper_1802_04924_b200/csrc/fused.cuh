@@ -30,6 +30,7 @@ template <class T> struct FusedWave {
   int32_t narrow; // run by the first cluster alone (cluster barrier to a narrow successor)
   int32_t n_chains; // > 0: a chain segment (several waves), items = its row groups
   const ChainDesc *chains;
+  int64_t stage;    // chain segment: bytes per staging buffer
   const FoldDesc<T> *cfolds;
 };
 
@@ -90,7 +91,7 @@ __device__ __forceinline__ void stage_item(const FusedWave<T> &W, int ready, Pan
   }
 }
 
-template <class T> __global__ void __launch_bounds__(kFusedThreads) dp_fused_kernel(FusedArgs<T> a) {
+template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_kernel(FusedArgs<T> a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   // dynamic: max(WaveSmem, the largest chain item) bytes
@@ -145,7 +146,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads) dp_fused_ker
     uint64_t *tr = a.trace && b0 == 0 ? a.trace + 16 * w : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = global_ns();
     if (W.n_chains)
-      for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x) chain_item<T>(W.chains, W.n_chains, W.cfolds, it, fused_smem);
+      for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x) chain_item<T>(W.chains, W.n_chains, W.cfolds, it, fused_smem, static_cast<size_t>(W.stage));
     else if (!narrow || static_cast<int>(blockIdx.x) < a.nc)
       for (int64_t it = b0; it < W.items; it += step)
         wave_item<T>(W.folds, W.nf, W.ftiles, W.merges, W.nm, it, sm, narrow ? nullptr : &st, it == 0 ? tr : nullptr);

@@ -75,8 +75,6 @@ struct ChainDesc {
   int32_t first, n;  // folds [first, first + n) of the segment's fold list
   int32_t nu, rows;  // t1 rows, rows per item
   int64_t item_begin;
-  int32_t buf;       // elements per staging buffer (w + padded t2 of any fold of the segment)
-  int32_t pad;
 };
 
 template <class T> union WaveSmem {
@@ -84,12 +82,19 @@ template <class T> union WaveSmem {
   PanelSmem<T> p;
 };
 
-// Shared memory of a chain item (dynamic, in elements of T unless noted):
-// A'[rows][kChainMax + 1] | cur[rows][kChainMax] | 2 x staging buffer
-// (w[nw] + t2[nw][nv + 1]) | the chain's fold descriptors.
-template <class T> __host__ __device__ constexpr size_t chain_smem_bytes(int rows, int buf, int max_len) {
-  return (static_cast<size_t>(rows) * (2 * kChainMax + 1) + 2 * static_cast<size_t>(buf)) * sizeof(T) + 16 +
-         static_cast<size_t>(max_len) * sizeof(FoldDesc<T>);
+// Shared memory of a chain item (dynamic, 16-byte-aligned sections):
+// 2 mbarriers | fold descriptors[max_len] | A'[rows][kChainMax + 1] |
+// cur[rows][kChainMax] | group minima (value, j)[kChainGroups][rows][kChainMax]
+// | 2 staging buffers (a fold's t2 bytes + w bytes, each 16-byte-rounded).
+constexpr int kChainGroups = kFoldThreads / 32; // j-groups = warps
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+template <class T> __host__ __device__ constexpr size_t chain_stage_bytes(int nw, int nv) {
+  return align16(static_cast<size_t>(nw) * nv * sizeof(T) + 16) + align16(static_cast<size_t>(nw) * sizeof(T) + 16);
+}
+template <class T> __host__ __device__ constexpr size_t chain_smem_bytes(int rows, int max_len, size_t stage) {
+  return 16 + align16(static_cast<size_t>(max_len) * sizeof(FoldDesc<T>)) +
+         align16(static_cast<size_t>(rows) * (2 * kChainMax + 1) * sizeof(T)) +
+         align16(static_cast<size_t>(kChainGroups) * rows * kChainMax * (sizeof(T) + 4)) + 2 * stage;
 }
 
 // A work item whose descriptor (and, for a panel tile, the operands the
@@ -263,28 +268,84 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Stages fold f's w and t2 (rows padded to nv + 1) into buf, asynchronously.
-template <class T> __device__ __forceinline__ void chain_stage(const FoldDesc<T> &f, T *buf) {
-  for (int j = threadIdx.x; j < f.nw; j += kFoldThreads) cp_async(buf + j, f.w + j);
-  T *t2s = buf + f.nw;
-  const int per = max(1, kFoldThreads / f.nv);
-  const int jr = threadIdx.x / f.nv, v = threadIdx.x - jr * f.nv;
-  if (jr < per)
-    for (int j = jr; j < f.nw; j += per) cp_async(t2s + j * (f.nv + 1) + v, f.t2 + static_cast<int64_t>(j) * f.nv + v);
-  cp_async_commit();
+// ---- bulk async copies (TMA, non-tensor) into shared memory ---------------
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t *bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Copies the 16-byte-rounded byte range of [p, p + n) to dst; returns the
+// element offset of p inside dst.  (Device allocations are whole 256-byte
+// granules, so the rounded range stays inside p's allocation.)
+template <class T> __device__ __forceinline__ unsigned bulk_range(T *dst, const T *p, int64_t n, uint64_t *bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p), lo = a & ~uintptr_t(15);
+  const uintptr_t hi = (a + static_cast<uintptr_t>(n) * sizeof(T) + 15) & ~uintptr_t(15);
+  bulk_g2s(dst, reinterpret_cast<const void *>(lo), static_cast<unsigned>(hi - lo), bar);
+  return static_cast<unsigned>((a - lo) / sizeof(T));
+}
+template <class T> __device__ __forceinline__ unsigned bulk_bytes(const T *p, int64_t n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p), lo = a & ~uintptr_t(15);
+  return static_cast<unsigned>(((a + static_cast<uintptr_t>(n) * sizeof(T) + 15) & ~uintptr_t(15)) - lo);
+}
+
+// Thread 0: stream fold f's t2 and w into staging buffer `buf` (t2 at the
+// front, w after it at `w_at` bytes), completing on `bar`.
+template <class T>
+__device__ __forceinline__ void chain_stage(const FoldDesc<T> &f, unsigned char *buf, size_t w_at, uint64_t *bar) {
+  const int64_t n2 = static_cast<int64_t>(f.nw) * f.nv;
+  fence_proxy_async(); // earlier generic reads of buf happen before the async writes
+  mbar_expect_tx(bar, bulk_bytes(f.t2, n2) + bulk_bytes(f.w, f.nw));
+  bulk_range(reinterpret_cast<T *>(buf), f.t2, n2, bar);
+  bulk_range(reinterpret_cast<T *>(buf + w_at), f.w, f.nw, bar);
+}
+
+// Keeps (v, j) if it precedes (bv, bj): lower value, then lower j.
+template <class T> __device__ __forceinline__ void keep_min_v(T v, int j, T &bv, int &bj) {
+  const bool t = v < bv || (v == bv && j < bj);
+  bv = t ? v : bv;
+  bj = t ? j : bj;
 }
 
 // Item `it` of a chain segment: rows [r0, r0 + rows) of one chain, through
-// all its folds.  Fold k + 1's w and t2 stream into shared memory (cp.async)
-// while fold k computes; its rows live in shared memory between folds.  Per
-// fold: A' = w + t1 rows (the reference's first addition), then threads =
-// (row, col) cells x G j-groups (adjacent lanes) scan j = g, g + G, ... and a
-// shuffle tree merges the groups (lower value, then lower j: the reference's
-// ascending strict-< scan).  Writes every fold's argmins and the last fold's
-// table; the intermediate tables have no other reader.
+// all its folds; the rows live in shared memory between folds, and fold
+// k + 1's t2 and w stream in (two bulk copies, mbarrier-completed) while
+// fold k scans.  Per fold: A' = w + t1 rows (the reference's first
+// addition); warp g of the rows' warps scans j = g, g + G, ... over the
+// row's cells (lane l: cells l, l + 32, ...: conflict-free reads of the
+// unpadded t2 rows), strict < in ascending j keeping the lowest j; the G
+// group minima then merge per cell (lower value, then lower j), so the
+// result is the reference's ascending strict-< scan.  Writes every fold's
+// argmins and the last fold's table; the intermediate tables have no other
+// reader.
 template <class T>
 __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains, const FoldDesc<T> *cf, int64_t it,
-                                           unsigned char *smem, uint64_t *tr = nullptr) {
+                                           unsigned char *smem, size_t stage, uint64_t *tr = nullptr) {
   const bool stamp = tr && threadIdx.x == 0;
   int lo = 0, hi = n_chains - 1;
   while (lo < hi) {
@@ -297,88 +358,131 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
   const ChainDesc c = chains[lo];
   const int r0 = static_cast<int>(it - c.item_begin) * c.rows;
   const int nr = min(c.rows, c.nu - r0);
-  T *A = reinterpret_cast<T *>(smem);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  unsigned char *p = smem + 16;
+  FoldDesc<T> *fd = reinterpret_cast<FoldDesc<T> *>(p);
+  p += align16(static_cast<size_t>(c.n) * sizeof(FoldDesc<T>));
+  T *A = reinterpret_cast<T *>(p);
   T *cur = A + c.rows * (kChainMax + 1);
-  T *buf[2] = {cur + c.rows * kChainMax, cur + c.rows * kChainMax + c.buf};
-  FoldDesc<T> *fd = reinterpret_cast<FoldDesc<T> *>(
-      (reinterpret_cast<uintptr_t>(buf[1] + c.buf) + 15) & ~uintptr_t(15));
+  p += align16(static_cast<size_t>(c.rows) * (2 * kChainMax + 1) * sizeof(T));
+  T *gv = reinterpret_cast<T *>(p);
+  int *gj = reinterpret_cast<int *>(gv + kChainGroups * c.rows * kChainMax);
+  p += align16(static_cast<size_t>(kChainGroups) * c.rows * kChainMax * (sizeof(T) + 4));
+  unsigned char *buf[2] = {p, p + stage};
   __syncthreads(); // the block's previous item may still read smem
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_proxy_async();
+  }
   for (int k = threadIdx.x; k < c.n; k += kFoldThreads) fd[k] = cf[c.first + k];
+  __syncthreads();
+  const size_t w_at0 = align16(static_cast<size_t>(fd[0].nw) * fd[0].nv * sizeof(T) + 16);
+  if (threadIdx.x == 0) chain_stage<T>(fd[0], buf[0], w_at0, &bar[0]);
   {
-    const FoldDesc<T> f0 = cf[c.first];
-    chain_stage<T>(f0, buf[0]);
+    const FoldDesc<T> &f0 = fd[0];
     for (int x = threadIdx.x; x < nr * f0.nw; x += kFoldThreads) {
       const int r = x / f0.nw, j = x - r * f0.nw;
       cur[r * kChainMax + j] = __ldcg(&f0.t1[static_cast<int64_t>(r0 + r) * f0.nw + j]);
     }
   }
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpr = kChainGroups / c.rows; // warps (j-groups) per row
   for (int k = 0; k < c.n; ++k) {
     const FoldDesc<T> &f = fd[k];
     const int nw = f.nw, nv = f.nv;
-    const T *bw = buf[k & 1], *t2s = bw + nw;
+    const size_t w_at = align16(static_cast<size_t>(nw) * nv * sizeof(T) + 16);
     if (stamp && k < 4) tr[4 * k] = trace_ns();
-    if (k + 1 < c.n) {
-      chain_stage<T>(fd[k + 1], buf[(k + 1) & 1]);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    if (k + 1 < c.n && threadIdx.x == 0) {
+      const size_t w_at1 = align16(static_cast<size_t>(fd[k + 1].nw) * fd[k + 1].nv * sizeof(T) + 16);
+      chain_stage<T>(fd[k + 1], buf[(k + 1) & 1], w_at1, &bar[(k + 1) & 1]);
     }
-    __syncthreads();
+    mbar_wait(&bar[k & 1], static_cast<unsigned>(k >> 1) & 1u);
+    const T *t2s = reinterpret_cast<const T *>(buf[k & 1]) +
+                   (reinterpret_cast<uintptr_t>(f.t2) & 15) / sizeof(T);
+    const T *ws = reinterpret_cast<const T *>(buf[k & 1] + w_at) + (reinterpret_cast<uintptr_t>(f.w) & 15) / sizeof(T);
     if (stamp && k < 4) tr[4 * k + 1] = trace_ns();
     for (int x = threadIdx.x; x < nr * nw; x += kFoldThreads) {
       const int r = x / nw, j = x - r * nw;
-      A[r * (kChainMax + 1) + j] = bw[j] + cur[r * kChainMax + j];
+      A[r * (kChainMax + 1) + j] = ws[j] + cur[r * kChainMax + j];
     }
     __syncthreads();
     if (stamp && k < 4) tr[4 * k + 2] = trace_ns();
-    const int cells = nr * nv;
-    int G = 1;
-    while (G < 32 && cells * G * 2 <= kFoldThreads) G *= 2;
-    const int g = threadIdx.x % G, slots = kFoldThreads / G;
-    const bool last = k + 1 == c.n;
-    for (int cell = threadIdx.x / G; cell < (cells + slots - 1) / slots * slots; cell += slots) {
-      const bool live = cell < cells;
-      const int r = live ? cell / nv : 0, v = live ? cell - r * nv : 0;
-      const T *a = A + r * (kChainMax + 1);
-      const T *t = t2s + v;
-      long long k0 = LLONG_MAX, k1 = LLONG_MAX;
-      int j0 = INT_MAX, j1 = INT_MAX;
-      if (live) {
+    { // scan: warp -> (row, j-group), lane -> cells lane, lane + 32, ...;
+      // two j per step into separate chains (2 x 4 independent compares)
+      const int r = warp / wpr, g = warp - r * wpr;
+      if (r < nr) {
+        const T *a = A + r * (kChainMax + 1);
+        int vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) vv[u] = min(lane + 32 * u, nv - 1); // clamped: dead cells re-read a live one
+        T b0[4], b1[4];
+        int j0[4], j1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b0[u] = b1[u] = T(0), j0[u] = j1[u] = INT_MAX;
         int j = g;
-        for (; j + 3 * G < nw; j += 4 * G) {
-          long long cc[4];
+        for (; j + wpr < nw; j += 2 * wpr) {
+          const T a0 = a[j], a1 = a[j + wpr];
+          const T *t0 = t2s + j * nv, *t1 = t0 + wpr * nv;
+          T x0[4], x1[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) cc[u] = scan_key<T>(a[j + u * G] + t[(j + u * G) * (nv + 1)]);
+          for (int u = 0; u < 4; ++u) x0[u] = t0[vv[u]], x1[u] = t1[vv[u]];
 #pragma unroll
-          for (int u = 0; u < 4; u += 2) {
-            if (cc[u] < k0) k0 = cc[u], j0 = j + u * G;
-            if (cc[u + 1] < k1) k1 = cc[u + 1], j1 = j + (u + 1) * G;
+          for (int u = 0; u < 4; ++u) {
+            const T c0 = a0 + x0[u], c1 = a1 + x1[u];
+            if (j0[u] == INT_MAX || c0 < b0[u]) b0[u] = c0, j0[u] = j;
+            if (j1[u] == INT_MAX || c1 < b1[u]) b1[u] = c1, j1[u] = j + wpr;
           }
         }
-        for (; j < nw; j += G) {
-          const long long c0 = scan_key<T>(a[j] + t[j * (nv + 1)]);
-          if (c0 < k0) k0 = c0, j0 = j;
+        if (j < nw) {
+          const T a0 = a[j];
+          const T *t0 = t2s + j * nv;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const T c0 = a0 + t0[vv[u]];
+            if (j0[u] == INT_MAX || c0 < b0[u]) b0[u] = c0, j0[u] = j;
+          }
         }
-        keep_min(k1, j1, k0, j0);
-      }
-      for (int o = G / 2; o > 0; o >>= 1) {
-        const long long ok = __shfl_xor_sync(0xffffffffu, k0, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, j0, o);
-        keep_min(ok, oj, k0, j0);
-      }
-      if (live && g == 0) {
-        const T val = a[j0] + t[j0 * (nv + 1)];
-        const int64_t o = static_cast<int64_t>(r0 + r) * nv + v;
-        f.am[o] = static_cast<uint16_t>(j0);
-        if (last)
-          f.out[o] = val;
-        else
-          cur[r * kChainMax + v] = val;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (j1[u] != INT_MAX) keep_min_v<T>(b1[u], j1[u], b0[u], j0[u]);
+          const int v = lane + 32 * u;
+          if (v < nv) {
+            gv[(g * c.rows + r) * kChainMax + v] = b0[u];
+            gj[(g * c.rows + r) * kChainMax + v] = j0[u];
+          }
+        }
       }
     }
     __syncthreads();
     if (stamp && k < 4) tr[4 * k + 3] = trace_ns();
+    const bool last = k + 1 == c.n;
+    const int ng = min(wpr, nw); // groups that scanned anything
+    for (int x = threadIdx.x; x < nr * nv; x += kFoldThreads) {
+      const int r = x / nv, v = x - r * nv;
+      T gvl[kChainGroups];
+      int gjl[kChainGroups];
+#pragma unroll
+      for (int g = 0; g < kChainGroups; ++g)
+        if (g < ng) gvl[g] = gv[(g * c.rows + r) * kChainMax + v], gjl[g] = gj[(g * c.rows + r) * kChainMax + v];
+      T b = gvl[0];
+      int j = gjl[0];
+#pragma unroll
+      for (int g = 1; g < kChainGroups; ++g)
+        if (g < ng) keep_min_v<T>(gvl[g], gjl[g], b, j);
+      const int64_t o = static_cast<int64_t>(r0 + r) * nv + v;
+      f.am[o] = static_cast<uint16_t>(j);
+      if (last)
+        f.out[o] = b;
+      else
+        cur[r * kChainMax + v] = b;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mbar_inval(&bar[0]);
+    mbar_inval(&bar[1]);
   }
 }
 

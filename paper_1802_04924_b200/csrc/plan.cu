@@ -15,6 +15,7 @@
 #include "minplus.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cstring>
 #include <functional>
@@ -489,7 +490,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       std::vector<ChainDesc> chains;
       std::vector<FoldDesc<T>> cf;
       int64_t items;
-      size_t smem = 0; // dynamic shared memory of its items
+      size_t smem = 0;  // dynamic shared memory of its items
+      size_t stage = 0; // bytes per staging buffer
     };
     std::vector<Segment> segs;
     std::vector<int> seg_of(static_cast<size_t>(nwv) + 2, -1);
@@ -500,7 +502,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         for (size_t q = wr.f0; q < wr.f0 + static_cast<size_t>(wr.nf); ++q) {
           const FoldOps &o = fold_ops[q];
           if (folds[q].nw > kChainMax || folds[q].nv > kChainMax) return false;
-          if (chain_smem_bytes<T>(1, folds[q].nw * (folds[q].nv + 2), 64) > kChainSmemMax) return false;
+          if (chain_smem_bytes<T>(1, 64, chain_stage_bytes<T>(folds[q].nw, folds[q].nv)) > kChainSmemMax) return false;
           if (prod_wave[static_cast<size_t>(o.e2)] >= ws) return false;
           const int p1 = prod_wave[static_cast<size_t>(o.e1)];
           if (p1 >= ws && p1 >= w) return false;
@@ -512,7 +514,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         if (fits(w, w))
           while (we + 1 <= nwv && fits(we + 1, w)) ++we;
         if (we > w) {
-          Segment sg{w, we, {}, {}, 0, 0};
+          Segment sg{w, we, {}, {}, 0, 0, 0};
           std::vector<int> chain_of_table(static_cast<size_t>(E_total), -1);
           std::vector<std::vector<size_t>> members;
           for (int x = w; x <= we; ++x) {
@@ -529,20 +531,21 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             }
           }
           int64_t rows_total = 0;
-          int buf = 0, max_len = 0;
+          int max_len = 0;
+          size_t stage = 0;
           for (const auto &m : members) {
             rows_total += folds[m.front()].nu;
             max_len = std::max(max_len, static_cast<int>(m.size()));
-            for (size_t q : m) buf = std::max(buf, folds[q].nw * (folds[q].nv + 2));
+            for (size_t q : m) stage = std::max(stage, chain_stage_bytes<T>(folds[q].nw, folds[q].nv));
           }
-          buf = (buf + 3) & ~3; // keeps the second buffer 16-byte aligned
           const int64_t cap = 2 * int64_t(ctx->sms);
           int rows = static_cast<int>(std::clamp<int64_t>((rows_total + cap - 1) / cap, 1, kChainRows));
-          while (rows > 1 && chain_smem_bytes<T>(rows, buf, max_len) > kChainSmemMax) --rows;
-          sg.smem = chain_smem_bytes<T>(rows, buf, max_len);
+          while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage) > kChainSmemMax) --rows;
+          sg.smem = chain_smem_bytes<T>(rows, max_len, stage);
+          sg.stage = stage;
           for (const auto &m : members) {
             ChainDesc cd{static_cast<int32_t>(sg.cf.size()), static_cast<int32_t>(m.size()), folds[m.front()].nu, rows,
-                         sg.items, buf, 0};
+                         sg.items};
             for (size_t q : m) sg.cf.push_back(folds[q]);
             sg.items += (cd.nu + rows - 1) / rows;
             sg.chains.push_back(cd);
@@ -627,6 +630,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           FusedWave<T> e{};
           e.items = S.items;
           e.n_chains = static_cast<int32_t>(S.chains.size());
+          e.stage = static_cast<int64_t>(S.stage);
           e.chains = reinterpret_cast<const ChainDesc *>(db + off_image + oc);
           e.cfolds = reinterpret_cast<const FoldDesc<T> *>(db + off_image + of);
           fw.push_back(e);
@@ -896,9 +900,17 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       P->phase_chain = im.phase_chain;
       const size_t dyn = im.dyn_smem;
       {
+        // grow the dynamic allowance monotonically; keep the shared-memory
+        // carveout at what two co-resident blocks need (the rest stays L1,
+        // which the table build and the wave folds lean on)
         static size_t dyn_set[2] = {0, 0};
         if (dyn_set[sizeof(T) == 8] < dyn) {
           PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+          cudaFuncAttributes fa_{};
+          PP_CUDA(cudaFuncGetAttributes(&fa_, dp_fused_kernel<T>));
+          const double need = 2.0 * static_cast<double>(dyn + fa_.sharedSizeBytes + 1024);
+          const int pct = std::min(100, static_cast<int>(std::ceil(100.0 * need / (228.0 * 1024))));
+          PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
           dyn_set[sizeof(T) == 8] = dyn;
         }
       }

@@ -4,19 +4,22 @@
 #include "kernels.cuh"
 #include <cstdio>
 #include <vector>
+#include <cstring>
+#include <unistd.h>
 using namespace pp;
 
-__global__ void k(const ChainDesc *chains, const FoldDesc<double> *cf, int items, long long *cyc, uint64_t *tr) {
+__global__ void k(const ChainDesc *chains, const FoldDesc<double> *cf, int items, long long *cyc, uint64_t *tr, size_t stage) {
   extern __shared__ __align__(16) unsigned char smem[];
   long long t0 = clock64();
-  for (int it = blockIdx.x; it < items; it += gridDim.x) chain_item<double>(chains, 1, cf, it, smem, blockIdx.x == 0 ? tr : nullptr);
+  for (int it = blockIdx.x; it < items; it += gridDim.x) chain_item<double>(chains, 1, cf, it, smem, stage, blockIdx.x == 0 ? tr : nullptr);
   long long t1 = clock64();
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
 }
 
 int main(int argc, char **argv) {
-  const int n = 19, nu = 53, nw = 80, nv = 80;
   const int rows = argc > 1 ? atoi(argv[1]) : 1;
+  const int n = argc > 2 ? atoi(argv[2]) : 19, nu = 53;
+  const int nw = argc > 3 ? atoi(argv[3]) : 80, nv = nw;
   std::vector<double> h(static_cast<size_t>(n) * (nw * nv + nw) + nu * nw);
   for (size_t i = 0; i < h.size(); ++i) h[i] = ((i * 7919) % 1000) * 0.001;
   double *d, *out;
@@ -38,28 +41,38 @@ int main(int argc, char **argv) {
   FoldDesc<double> *df;
   cudaMalloc(&df, n * sizeof(FoldDesc<double>));
   cudaMemcpy(df, f.data(), n * sizeof(FoldDesc<double>), cudaMemcpyHostToDevice);
-  const int buf = (nw * (nv + 2) + 3) & ~3;
-  ChainDesc c{0, n, nu, rows, 0, buf, 0};
+  ChainDesc c{0, n, nu, rows, 0};
   ChainDesc *dc;
   cudaMalloc(&dc, sizeof(c));
   cudaMemcpy(dc, &c, sizeof(c), cudaMemcpyHostToDevice);
-  const size_t sm = chain_smem_bytes<double>(rows, buf, n);
+  const size_t stage = chain_stage_bytes<double>(nw, nv);
+  const size_t sm = chain_smem_bytes<double>(rows, n, stage);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   long long *cyc;
   cudaMalloc(&cyc, 8);
   const int items = (nu + rows - 1) / rows;
   uint64_t *tr;
-  cudaMalloc(&tr, 16 * 8);
-  for (int r = 0; r < 3; ++r) k<<<items, 256, sm>>>(dc, df, items, cyc, tr);
+  cudaHostAlloc(&tr, 16 * 8, cudaHostAllocMapped);
+  memset(tr, 0, 128);
+  k<<<items, 256, sm>>>(dc, df, items, cyc, tr, stage);
+  for (int spin = 0; spin < 20 && cudaStreamQuery(0) == cudaErrorNotReady; ++spin) usleep(100000);
+  if (cudaStreamQuery(0) == cudaErrorNotReady) {
+    printf("HANG: stamps");
+    for (int q = 0; q < 16; ++q) printf(" %llu", (unsigned long long)((volatile uint64_t *)tr)[q]);
+    printf("\n");
+    fflush(stdout);
+    _exit(3);
+  }
+  for (int r = 0; r < 2; ++r) k<<<items, 256, sm>>>(dc, df, items, cyc, tr, stage);
   cudaError_t e = cudaDeviceSynchronize();
   long long hc;
   cudaMemcpy(&hc, cyc, 8, cudaMemcpyDeviceToHost);
   printf("rows %d smem %zu: %s, %.0f cycles per fold (%.2f us at 1.9 GHz)\n", rows, sm, cudaGetErrorString(e), hc / double(n),
          hc / double(n) / 1900.0);
   uint64_t t[16];
-  cudaMemcpy(t, tr, 128, cudaMemcpyDeviceToHost);
-  for (int q = 1; q < 4; ++q)
-    printf("fold %d: stage+wait %lld  A' %lld  scan %lld  (total %lld cycles)\n", q, (long long)(t[4 * q + 1] - t[4 * q]),
-           (long long)(t[4 * q + 2] - t[4 * q + 1]), (long long)(t[4 * q + 3] - t[4 * q + 2]), (long long)(t[4 * q + 3] - t[4 * q]));
+  memcpy(t, tr, 128);
+  for (int q = 1; q < 3; ++q)
+    printf("fold %d: wait %lld  A' %lld  scan %lld  (total %lld cycles)\n", q, (long long)(t[4 * q + 1] - t[4 * q]),
+           (long long)(t[4 * q + 2] - t[4 * q + 1]), (long long)(t[4 * q + 3] - t[4 * q + 2]), (long long)(t[4 * (q + 1)] - t[4 * q]));
   return 0;
 }
