@@ -75,6 +75,10 @@ struct ChainDesc {
   int32_t first, n;  // folds [first, first + n) of the segment's fold list
   int32_t nu, rows;  // t1 rows, rows per item
   int64_t item_begin;
+  // optional unwind path table [nu][nv of the last fold][n]: entry k = the
+  // argmin of fold k along the chain's backtrack from (row, final column), so
+  // the finish phase assigns the whole chain with one lookup
+  uint16_t *path;
 };
 
 template <class T> union WaveSmem {
@@ -91,10 +95,11 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 template <class T> __host__ __device__ constexpr size_t chain_stage_bytes(int nw, int nv) {
   return align16(static_cast<size_t>(nw) * nv * sizeof(T) + 16) + align16(static_cast<size_t>(nw) * sizeof(T) + 16);
 }
-template <class T> __host__ __device__ constexpr size_t chain_smem_bytes(int rows, int max_len, size_t stage) {
+template <class T> __host__ __device__ constexpr size_t chain_smem_bytes(int rows, int max_len, size_t stage, bool path) {
   return 16 + align16(static_cast<size_t>(max_len) * sizeof(FoldDesc<T>)) +
          align16(static_cast<size_t>(rows) * (2 * kChainMax + 1) * sizeof(T)) +
-         align16(static_cast<size_t>(kChainGroups) * rows * kChainMax * (sizeof(T) + 4)) + 2 * stage;
+         align16(static_cast<size_t>(kChainGroups) * rows * kChainMax * (sizeof(T) + 4)) + 2 * stage +
+         (path ? align16(static_cast<size_t>(max_len) * rows * kChainMax * 2) : 0);
 }
 
 // A work item whose descriptor (and, for a panel tile, the operands the
@@ -332,6 +337,51 @@ template <class T> __device__ __forceinline__ void keep_min_v(T v, int j, T &bv,
   bj = t ? j : bj;
 }
 
+// One warp's share of a chain fold: cells lane + 32u (u < U) of one row, the
+// j values g, g + G, ... two per step into separate chains; A'[j] = w[j] +
+// row[j] (the reference's first addition) is formed on the fly.  Writes the
+// per-cell (value, j) minima of this j-group.
+template <class T, int U>
+__device__ __forceinline__ void chain_scan(const T *ws, const T *cr, const T *t2s, int nw, int nv, int g, int G, int lane,
+                                           T *ogv, int *ogj) {
+  int vv[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) vv[u] = min(lane + 32 * u, nv - 1); // clamped: dead cells re-read a live one
+  T b0[U], b1[U];
+  int j0[U], j1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) b0[u] = b1[u] = T(0), j0[u] = j1[u] = INT_MAX;
+  int j = g;
+  for (; j + G < nw; j += 2 * G) {
+    const T a0 = ws[j] + cr[j], a1 = ws[j + G] + cr[j + G];
+    const T *t0 = t2s + j * nv, *t1 = t0 + G * nv;
+    T x0[U], x1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x0[u] = t0[vv[u]], x1[u] = t1[vv[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const T c0 = a0 + x0[u], c1 = a1 + x1[u];
+      if (j0[u] == INT_MAX || c0 < b0[u]) b0[u] = c0, j0[u] = j;
+      if (j1[u] == INT_MAX || c1 < b1[u]) b1[u] = c1, j1[u] = j + G;
+    }
+  }
+  if (j < nw) {
+    const T a0 = ws[j] + cr[j];
+    const T *t0 = t2s + j * nv;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const T c0 = a0 + t0[vv[u]];
+      if (j0[u] == INT_MAX || c0 < b0[u]) b0[u] = c0, j0[u] = j;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (j1[u] != INT_MAX) keep_min_v<T>(b1[u], j1[u], b0[u], j0[u]);
+    const int v = lane + 32 * u;
+    if (v < nv) ogv[v] = b0[u], ogj[v] = j0[u];
+  }
+}
+
 // Item `it` of a chain segment: rows [r0, r0 + rows) of one chain, through
 // all its folds; the rows live in shared memory between folds, and fold
 // k + 1's t2 and w stream in (two bulk copies, mbarrier-completed) while
@@ -369,6 +419,7 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
   int *gj = reinterpret_cast<int *>(gv + kChainGroups * c.rows * kChainMax);
   p += align16(static_cast<size_t>(kChainGroups) * c.rows * kChainMax * (sizeof(T) + 4));
   unsigned char *buf[2] = {p, p + stage};
+  uint16_t *amS = reinterpret_cast<uint16_t *>(p + 2 * stage); // [n][rows][kChainMax] when c.path
   __syncthreads(); // the block's previous item may still read smem
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -377,8 +428,11 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
   }
   for (int k = threadIdx.x; k < c.n; k += kFoldThreads) fd[k] = cf[c.first + k];
   __syncthreads();
-  const size_t w_at0 = align16(static_cast<size_t>(fd[0].nw) * fd[0].nv * sizeof(T) + 16);
-  if (threadIdx.x == 0) chain_stage<T>(fd[0], buf[0], w_at0, &bar[0]);
+  auto w_at = [&](int k) { return align16(static_cast<size_t>(fd[k].nw) * fd[k].nv * sizeof(T) + 16); };
+  if (threadIdx.x == 0) { // folds 0 and 1 stream in now; fold k + 2 once fold k's scan frees its buffer
+    chain_stage<T>(fd[0], buf[0], w_at(0), &bar[0]);
+    if (c.n > 1) chain_stage<T>(fd[1], buf[1], w_at(1), &bar[1]);
+  }
   {
     const FoldDesc<T> &f0 = fd[0];
     for (int x = threadIdx.x; x < nr * f0.nw; x += kFoldThreads) {
@@ -392,71 +446,32 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
   for (int k = 0; k < c.n; ++k) {
     const FoldDesc<T> &f = fd[k];
     const int nw = f.nw, nv = f.nv;
-    const size_t w_at = align16(static_cast<size_t>(nw) * nv * sizeof(T) + 16);
     if (stamp && k < 4) tr[4 * k] = trace_ns();
-    if (k + 1 < c.n && threadIdx.x == 0) {
-      const size_t w_at1 = align16(static_cast<size_t>(fd[k + 1].nw) * fd[k + 1].nv * sizeof(T) + 16);
-      chain_stage<T>(fd[k + 1], buf[(k + 1) & 1], w_at1, &bar[(k + 1) & 1]);
-    }
     mbar_wait(&bar[k & 1], static_cast<unsigned>(k >> 1) & 1u);
-    const T *t2s = reinterpret_cast<const T *>(buf[k & 1]) +
-                   (reinterpret_cast<uintptr_t>(f.t2) & 15) / sizeof(T);
-    const T *ws = reinterpret_cast<const T *>(buf[k & 1] + w_at) + (reinterpret_cast<uintptr_t>(f.w) & 15) / sizeof(T);
-    if (stamp && k < 4) tr[4 * k + 1] = trace_ns();
-    for (int x = threadIdx.x; x < nr * nw; x += kFoldThreads) {
-      const int r = x / nw, j = x - r * nw;
-      A[r * (kChainMax + 1) + j] = ws[j] + cur[r * kChainMax + j];
-    }
-    __syncthreads();
-    if (stamp && k < 4) tr[4 * k + 2] = trace_ns();
-    { // scan: warp -> (row, j-group), lane -> cells lane, lane + 32, ...;
-      // two j per step into separate chains (2 x 4 independent compares)
+    const T *t2s = reinterpret_cast<const T *>(buf[k & 1]) + (reinterpret_cast<uintptr_t>(f.t2) & 15) / sizeof(T);
+    const T *ws = reinterpret_cast<const T *>(buf[k & 1] + w_at(k)) + (reinterpret_cast<uintptr_t>(f.w) & 15) / sizeof(T);
+    if (stamp && k < 4) tr[4 * k + 1] = tr[4 * k + 2] = trace_ns();
+    { // scan: warp -> (row, j-group), lane -> cells lane, lane + 32, ...
       const int r = warp / wpr, g = warp - r * wpr;
       if (r < nr) {
-        const T *a = A + r * (kChainMax + 1);
-        int vv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) vv[u] = min(lane + 32 * u, nv - 1); // clamped: dead cells re-read a live one
-        T b0[4], b1[4];
-        int j0[4], j1[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) b0[u] = b1[u] = T(0), j0[u] = j1[u] = INT_MAX;
-        int j = g;
-        for (; j + wpr < nw; j += 2 * wpr) {
-          const T a0 = a[j], a1 = a[j + wpr];
-          const T *t0 = t2s + j * nv, *t1 = t0 + wpr * nv;
-          T x0[4], x1[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x0[u] = t0[vv[u]], x1[u] = t1[vv[u]];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const T c0 = a0 + x0[u], c1 = a1 + x1[u];
-            if (j0[u] == INT_MAX || c0 < b0[u]) b0[u] = c0, j0[u] = j;
-            if (j1[u] == INT_MAX || c1 < b1[u]) b1[u] = c1, j1[u] = j + wpr;
-          }
-        }
-        if (j < nw) {
-          const T a0 = a[j];
-          const T *t0 = t2s + j * nv;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const T c0 = a0 + t0[vv[u]];
-            if (j0[u] == INT_MAX || c0 < b0[u]) b0[u] = c0, j0[u] = j;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (j1[u] != INT_MAX) keep_min_v<T>(b1[u], j1[u], b0[u], j0[u]);
-          const int v = lane + 32 * u;
-          if (v < nv) {
-            gv[(g * c.rows + r) * kChainMax + v] = b0[u];
-            gj[(g * c.rows + r) * kChainMax + v] = j0[u];
-          }
+        T *ogv = gv + (g * c.rows + r) * kChainMax;
+        int *ogj = gj + (g * c.rows + r) * kChainMax;
+        const T *cr = cur + r * kChainMax;
+        switch ((nv + 31) >> 5) {
+        case 1: chain_scan<T, 1>(ws, cr, t2s, nw, nv, g, wpr, lane, ogv, ogj); break;
+        case 2: chain_scan<T, 2>(ws, cr, t2s, nw, nv, g, wpr, lane, ogv, ogj); break;
+        case 3: chain_scan<T, 3>(ws, cr, t2s, nw, nv, g, wpr, lane, ogv, ogj); break;
+        default: chain_scan<T, 4>(ws, cr, t2s, nw, nv, g, wpr, lane, ogv, ogj); break;
         }
       }
     }
     __syncthreads();
     if (stamp && k < 4) tr[4 * k + 3] = trace_ns();
+    if (k + 2 < c.n && threadIdx.x == kFoldThreads - 1) { // buf[k & 1] is free again
+      if (tr && k < 4) tr[16 + 2 * k] = trace_ns();
+      chain_stage<T>(fd[k + 2], buf[k & 1], w_at(k + 2), &bar[k & 1]);
+      if (tr && k < 4) tr[17 + 2 * k] = trace_ns();
+    }
     const bool last = k + 1 == c.n;
     const int ng = min(wpr, nw); // groups that scanned anything
     for (int x = threadIdx.x; x < nr * nv; x += kFoldThreads) {
@@ -473,12 +488,26 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
         if (g < ng) keep_min_v<T>(gvl[g], gjl[g], b, j);
       const int64_t o = static_cast<int64_t>(r0 + r) * nv + v;
       f.am[o] = static_cast<uint16_t>(j);
+      if (c.path) amS[(k * c.rows + r) * kChainMax + v] = static_cast<uint16_t>(j);
       if (last)
         f.out[o] = b;
       else
         cur[r * kChainMax + v] = b;
     }
     __syncthreads();
+  }
+  if (c.path) { // backtrack every (row, final column) through the chain
+    const int nvl = fd[c.n - 1].nv;
+    for (int x = threadIdx.x; x < nr * nvl; x += kFoldThreads) {
+      const int r = x / nvl, v = x - r * nvl;
+      uint16_t *out = c.path + (static_cast<int64_t>(r0 + r) * nvl + v) * c.n;
+      int col = v;
+      for (int k = c.n - 1; k >= 0; --k) {
+        const uint16_t j = amS[(k * c.rows + r) * kChainMax + col];
+        out[k] = j;
+        col = j;
+      }
+    }
   }
   if (threadIdx.x == 0) {
     mbar_inval(&bar[0]);
@@ -747,8 +776,10 @@ __global__ void __launch_bounds__(kEnumThreads)
 }
 
 struct UnwindRec {
-  const uint16_t *am;
+  const uint16_t *am; // argmins [rows][cols]; a chain record: path table [rows][cols][n]
   int32_t removed, src, dst, cols;
+  int32_t n;          // 0: one fold; n > 0: a chain of n folds whose removed nodes are chain_nodes[removed, removed + n)
+  int32_t pad;
 };
 
 struct FinishArgs {
@@ -765,6 +796,7 @@ struct FinishArgs {
   // first; group g = recs[group_begin[g], group_begin[g+1])
   const UnwindRec *recs;
   int n_rec;
+  const int32_t *chain_nodes;
   const int32_t *group_begin;
   int n_groups;
   double *terms; // [nl + ne] scratch
@@ -779,6 +811,7 @@ struct FinishArgs {
   const int32_t *esrc, *edst, *counts;
   int ne;
   double *cost;
+  uint64_t *trace; // optional: stamps after each finish step (profiling)
 };
 
 constexpr int kFinishThreads = 256;
@@ -799,6 +832,8 @@ template <class T> __global__ void __launch_bounds__(kFinishThreads) finish_kern
 
 template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a) {
   using A = typename Acc<T>::type;
+  const bool stamp = a.trace && threadIdx.x == 0;
+  if (stamp) a.trace[0] = trace_ns();
   __shared__ A sv[kFinishThreads];
   __shared__ int64_t si[kFinishThreads];
   const A *bv = static_cast<const A *>(a.blk_val);
@@ -831,6 +866,7 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
     }
     *a.final_cost = ldexp(static_cast<double>(sv[0]), -a.shift);
   }
+  if (stamp) a.trace[1] = trace_ns();
   if (a.n_rec < 0) return;
   __syncthreads();
   for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) a.indices[l] = -1;
@@ -840,10 +876,17 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
   for (int gidx = 0; gidx < a.n_groups; ++gidx) { // waves, last first
     for (int q = a.group_begin[gidx] + threadIdx.x; q < a.group_begin[gidx + 1]; q += kFinishThreads) {
       const UnwindRec u = a.recs[q];
-      a.indices[u.removed] = u.am[static_cast<int64_t>(a.indices[u.src]) * u.cols + a.indices[u.dst]];
+      const int64_t at = static_cast<int64_t>(a.indices[u.src]) * u.cols + a.indices[u.dst];
+      if (u.n == 0) {
+        a.indices[u.removed] = u.am[at];
+      } else {
+        const uint16_t *pth = u.am + at * u.n;
+        for (int k = 0; k < u.n; ++k) a.indices[a.chain_nodes[u.removed + k]] = pth[k];
+      }
     }
     __syncthreads();
   }
+  if (stamp) a.trace[2] = trace_ns();
   const T *onode = static_cast<const T *>(a.onode);
   const T *oxfer = static_cast<const T *>(a.oxfer);
   for (int l = threadIdx.x; l < a.nl; l += kFinishThreads)
@@ -859,12 +902,14 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
     for (int x = 0; x < a.nl + a.ne; ++x) t += a.terms[x];
     *a.cost = t;
   }
+  if (stamp) a.trace[3] = trace_ns();
   if (a.host_res) { // zero-copy: results straight into pinned host memory
     __syncthreads();
     for (size_t b = threadIdx.x; b < a.res_bytes / 4; b += kFinishThreads)
       reinterpret_cast<volatile uint32_t *>(a.host_res)[b] = reinterpret_cast<const uint32_t *>(a.dev_res)[b];
     __threadfence_system();
   }
+  if (stamp) a.trace[4] = trace_ns();
 }
 
 template <class T> __global__ void to_double_kernel(const T *in, double *out, int64_t n, int shift) {

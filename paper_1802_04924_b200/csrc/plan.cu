@@ -319,7 +319,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<WaveRange> waves;
     std::vector<std::tuple<const void *, void *, size_t>> final_gathers; // sharded: final edges + argmins
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
-    size_t oG, oT, oFW, oST, oTR;
+    size_t oG, oT, oFW, oST, oTR, oCN;
     int n_phases = 0;                // fused kernel: waves / chain segments
     size_t dyn_smem = 0;             // fused kernel dynamic shared memory
     std::vector<char> phase_chain;   // phase is a chain segment
@@ -357,7 +357,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     auto amp = [&](int oi) { return reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]); };
     std::vector<FoldDesc<T>> folds;
     struct FoldOps {
-      int e1, e2, ne, wave;
+      int e1, e2, ne, wave, oi;
     };
     std::vector<FoldOps> fold_ops;
     std::vector<MergeDesc<T>> merges;
@@ -455,7 +455,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           f.small = small_wave ? (f.nw <= kPanel && env_int("PARPLAN_PANEL", 1) ? panel_mode : 1) : 0;
           const int ts = f.small >= kPanel16 ? panel_side(f.small) : f.small ? kSmallTile : kTile;
           f.late = 0; // set below, once the narrow waves are known
-          fold_ops.push_back({op.e1, op.e2, op.ne, w});
+          fold_ops.push_back({op.e1, op.e2, op.ne, w, oi});
           f.tiles_k = (f.nv + ts - 1) / ts;
           f.tile_begin = wr.ftiles;
           wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
@@ -495,6 +495,15 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     };
     std::vector<Segment> segs;
     std::vector<int> seg_of(static_cast<size_t>(nwv) + 2, -1);
+    // chains with unwind path tables: one finish record each
+    struct ChainRec {
+      int node_off, n;
+      const uint16_t *path;
+    };
+    std::vector<ChainRec> chain_recs;
+    std::vector<int> chain_last_op;
+    std::vector<int32_t> chain_nodes;
+    std::vector<int> chain_of_op(s.ops.size(), -1);
     if (use_fused && env_int("PARPLAN_CHAINS", 1)) {
       auto fits = [&](int w, int ws) {
         const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
@@ -502,7 +511,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         for (size_t q = wr.f0; q < wr.f0 + static_cast<size_t>(wr.nf); ++q) {
           const FoldOps &o = fold_ops[q];
           if (folds[q].nw > kChainMax || folds[q].nv > kChainMax) return false;
-          if (chain_smem_bytes<T>(1, 64, chain_stage_bytes<T>(folds[q].nw, folds[q].nv)) > kChainSmemMax) return false;
+          if (chain_smem_bytes<T>(1, 64, chain_stage_bytes<T>(folds[q].nw, folds[q].nv), false) > kChainSmemMax) return false;
           if (prod_wave[static_cast<size_t>(o.e2)] >= ws) return false;
           const int p1 = prod_wave[static_cast<size_t>(o.e1)];
           if (p1 >= ws && p1 >= w) return false;
@@ -540,14 +549,27 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           }
           const int64_t cap = 2 * int64_t(ctx->sms);
           int rows = static_cast<int>(std::clamp<int64_t>((rows_total + cap - 1) / cap, 1, kChainRows));
-          while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage) > kChainSmemMax) --rows;
-          sg.smem = chain_smem_bytes<T>(rows, max_len, stage);
+          // unwind path tables for chains of >= 3 folds, when the argmins fit in shared memory
+          bool path = max_len >= 3 && env_int("PARPLAN_CHAIN_PATH", 1);
+          while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage, path) > kChainSmemMax) --rows;
+          if (path && chain_smem_bytes<T>(rows, max_len, stage, path) > kChainSmemMax) path = false;
+          sg.smem = chain_smem_bytes<T>(rows, max_len, stage, path);
           sg.stage = stage;
           for (const auto &m : members) {
             ChainDesc cd{static_cast<int32_t>(sg.cf.size()), static_cast<int32_t>(m.size()), folds[m.front()].nu, rows,
-                         sg.items};
+                         sg.items, nullptr};
             for (size_t q : m) sg.cf.push_back(folds[q]);
             sg.items += (cd.nu + rows - 1) / rows;
+            if (path && m.size() >= 3) { // path table inside the image (rewritten by every run)
+              const FoldDesc<T> &fl = folds[m.back()];
+              const size_t off = im.pk.put(std::vector<uint16_t>(static_cast<size_t>(cd.nu) * fl.nv * m.size()));
+              cd.path = reinterpret_cast<uint16_t *>(db + off_image + off);
+              ChainRec cr{static_cast<int>(chain_nodes.size()), static_cast<int>(m.size()), cd.path};
+              for (size_t q : m) chain_nodes.push_back(s.ops[static_cast<size_t>(fold_ops[q].oi)].removed);
+              for (size_t q : m) chain_of_op[static_cast<size_t>(fold_ops[q].oi)] = static_cast<int>(chain_recs.size());
+              chain_last_op.push_back(fold_ops[m.back()].oi);
+              chain_recs.push_back(cr);
+            }
             sg.chains.push_back(cd);
           }
           for (int x = w; x <= we; ++x) seg_of[static_cast<size_t>(x)] = static_cast<int>(segs.size());
@@ -605,7 +627,13 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         const int oi = s.exec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
         if (op.type) continue;
-        recs.push_back(UnwindRec{amfullp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)]});
+        const int ch = chain_of_op[static_cast<size_t>(oi)];
+        if (ch < 0) {
+          recs.push_back(UnwindRec{amfullp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)], 0, 0});
+        } else if (chain_last_op[static_cast<size_t>(ch)] == oi) { // the whole chain, at its last fold
+          const ChainRec &cr = chain_recs[static_cast<size_t>(ch)];
+          recs.push_back(UnwindRec{cr.path, cr.node_off, op.u, op.v, cols[static_cast<size_t>(op.ne)], cr.n, 0});
+        }
       }
       if (static_cast<int32_t>(recs.size()) > groups.back()) groups.push_back(static_cast<int32_t>(recs.size()));
     }
@@ -658,11 +686,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       im.phase_chain.clear();
       for (const auto &e : fw) im.phase_chain.push_back(e.n_chains > 0);
       im.oST = pk.put(std::vector<uint64_t>(fw.size() + 4));
-      im.oTR = env_int("PARPLAN_WAVE_TRACE", 0) ? pk.put(std::vector<uint64_t>(16 * fw.size())) : 0;
+      im.oTR = env_int("PARPLAN_WAVE_TRACE", 0) ? pk.put(std::vector<uint64_t>(16 * fw.size() + 16)) : 0;
     }
     im.oN = pk.put(en);
     im.oE = pk.put(ee);
     im.oR = pk.put(recs);
+    im.oCN = pk.put(chain_nodes.empty() ? std::vector<int32_t>{0} : chain_nodes);
     im.oL = pk.put(node_layer);
     im.oCO = pk.put(t.cat_off);
     im.oXO = pk.put(t.xoff);
@@ -853,6 +882,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.cost = fa.final_cost + 1;
     fa.shift = t.shift;
     fa.recs = reinterpret_cast<const UnwindRec *>(dimg + im.oR);
+    fa.chain_nodes = reinterpret_cast<const int32_t *>(dimg + im.oCN);
     fa.n_rec = static_cast<int>(s.node_ops);
     fa.group_begin = reinterpret_cast<const int32_t *>(dimg + im.oG);
     fa.n_groups = im.nG;
@@ -893,6 +923,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       fz.stamps = reinterpret_cast<uint64_t *>(dimg + im.oST);
       fz.stage = env_int("PARPLAN_STAGE", 1);
       fz.trace = im.oTR ? reinterpret_cast<uint64_t *>(dimg + im.oTR) : nullptr;
+      if (fz.trace) fz.fin.trace = fz.trace + 16 * im.n_phases;
       P->trace_off = im.oTR;
       P->stamp_off = im.oST;
       P->n_stamps = im.n_phases + 4; // start, tables, waves / segments..., enum, finish
@@ -1153,7 +1184,7 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
         PP_CUDA(cudaMemcpy(st.data(), P->dbase + P->image_off + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
         const int waves = P->n_stamps - 4;
         if (P->trace_off) {
-          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves));
+          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves + 16));
           PP_CUDA(cudaMemcpy(tr.data(), P->dbase + P->image_off + P->trace_off, tr.size() * 8, cudaMemcpyDeviceToHost));
           for (int w = 0; w < waves; ++w) {
             const uint64_t *r = &tr[static_cast<size_t>(16 * w)];
@@ -1164,6 +1195,10 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
                          "arrive %6.0f leave %6.0f ns\n",
                          w, rel(r[0]), rel(r[7]), rel(r[1]), rel(r[5]), rel(r[6]), rel(r[2]), rel(r[3]), rel(r[4]));
           }
+          const uint64_t *fr = &tr[static_cast<size_t>(16 * waves)];
+          std::fprintf(stderr, "finish: reduce %.0f unwind %.0f resum %.0f results %.0f ns\n",
+                       static_cast<double>(fr[1] - fr[0]), static_cast<double>(fr[2] - fr[1]),
+                       static_cast<double>(fr[3] - fr[2]), static_cast<double>(fr[4] - fr[3]));
         }
         for (int ph = 0; ph + 1 < P->n_stamps; ++ph) {
           const int pk = ph == 0       ? 11

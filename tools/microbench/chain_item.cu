@@ -46,14 +46,14 @@ int main(int argc, char **argv) {
   cudaMalloc(&dc, sizeof(c));
   cudaMemcpy(dc, &c, sizeof(c), cudaMemcpyHostToDevice);
   const size_t stage = chain_stage_bytes<double>(nw, nv);
-  const size_t sm = chain_smem_bytes<double>(rows, n, stage);
+  const size_t sm = chain_smem_bytes<double>(rows, n, stage, false);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   long long *cyc;
   cudaMalloc(&cyc, 8);
   const int items = (nu + rows - 1) / rows;
   uint64_t *tr;
-  cudaHostAlloc(&tr, 16 * 8, cudaHostAllocMapped);
-  memset(tr, 0, 128);
+  cudaHostAlloc(&tr, 32 * 8, cudaHostAllocMapped);
+  memset(tr, 0, 256);
   k<<<items, 256, sm>>>(dc, df, items, cyc, tr, stage);
   for (int spin = 0; spin < 20 && cudaStreamQuery(0) == cudaErrorNotReady; ++spin) usleep(100000);
   if (cudaStreamQuery(0) == cudaErrorNotReady) {
@@ -69,8 +69,10 @@ int main(int argc, char **argv) {
   cudaMemcpy(&hc, cyc, 8, cudaMemcpyDeviceToHost);
   printf("rows %d smem %zu: %s, %.0f cycles per fold (%.2f us at 1.9 GHz)\n", rows, sm, cudaGetErrorString(e), hc / double(n),
          hc / double(n) / 1900.0);
-  uint64_t t[16];
-  memcpy(t, tr, 128);
+  uint64_t t[32];
+  memcpy(t, tr, 256);
+  printf("stage issue: %lld %lld cycles; merge phase ends %lld after scan\n", (long long)(t[19] - t[18]), (long long)(t[21] - t[20]),
+         (long long)(t[8] - t[7]));
   for (int q = 1; q < 3; ++q)
     printf("fold %d: wait %lld  A' %lld  scan %lld  (total %lld cycles)\n", q, (long long)(t[4 * q + 1] - t[4 * q]),
            (long long)(t[4 * q + 2] - t[4 * q + 1]), (long long)(t[4 * q + 3] - t[4 * q + 2]), (long long)(t[4 * (q + 1)] - t[4 * q]));
