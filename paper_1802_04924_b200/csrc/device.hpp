@@ -117,7 +117,9 @@ struct pp_context {
   // grow-only pools for one-shot plans (pp_plan / pp_plan_with_tables): no
   // cudaMalloc/cudaFree on the steady-state path
   pp::DBuf<unsigned char> plan_pool;
+  pp::DBuf<unsigned char> plan_scratch; // device-only buffers of one-shot plans
   pp::PinnedBuf plan_pinned;
+  size_t last_image_bytes = 0;          // reserve hint for the next descriptor image
 
   void begin() const; // cudaSetDevice + record ev0
   double end_ms();    // record ev1, sync, elapsed

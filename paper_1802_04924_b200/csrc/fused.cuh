@@ -177,7 +177,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
     enum_block<T>(a.en, a.k, a.ee, a.m, a.space, a.per_thread, static_cast<A *>(a.blk_val), a.blk_idx, vb);
   grid.sync();
   if (stamp) a.stamps[ph++] = global_ns();
-  if (blockIdx.x == 0) finish_block<T>(a.fin);
+  if (blockIdx.x == 0) finish_block<T>(a.fin, fused_smem);
   if (stamp) a.stamps[ph++] = global_ns();
 }
 

@@ -812,6 +812,7 @@ struct FinishArgs {
   int ne;
   double *cost;
   uint64_t *trace; // optional: stamps after each finish step (profiling)
+  int32_t smem_ok;  // the caller's shared memory holds indices[nl] + terms[nl + ne]
 };
 
 constexpr int kFinishThreads = 256;
@@ -824,82 +825,137 @@ constexpr int kFinishThreads = 256;
 // independent and the CTA processes a wave in parallel (planner.hpp:309-319).
 // The cost terms are gathered in parallel, then summed by one thread in the
 // reference's order (cost.hpp:235-246) — bit-identical.
-template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a);
+template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a, unsigned char *smem = nullptr);
 
 template <class T> __global__ void __launch_bounds__(kFinishThreads) finish_kernel(FinishArgs a) {
   finish_block<T>(a);
 }
 
-template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a) {
+template <class A> __device__ __forceinline__ A shfl_xor_any(A v, int o) {
+  if constexpr (sizeof(A) == 8) {
+    long long x;
+    memcpy(&x, &v, 8);
+    x = __shfl_xor_sync(0xffffffffu, x, o);
+    memcpy(&v, &x, 8);
+    return v;
+  } else {
+    return __shfl_xor_sync(0xffffffffu, v, o);
+  }
+}
+
+// (value, linear index) order of the enumeration: lower value, then lower
+// index; INT64_MAX marks "no candidate".
+template <class A> __device__ __forceinline__ void keep_best(A ov, int64_t oi, A &bv, int64_t &bi) {
+  if (oi != INT64_MAX && (bi == INT64_MAX || ov < bv || (ov == bv && oi < bi))) bv = ov, bi = oi;
+}
+
+// Shared-memory layout of finish_block (when a.smem_ok): terms[nl + ne] |
+// cat_off[nl] | xoff[ne] (8-byte) | indices[nl] | counts[nl] | esrc[ne] |
+// edst[ne] | enumeration node counts[k] (4-byte).
+__host__ __device__ constexpr size_t finish_smem_bytes(int nl, int ne, int k) {
+  return static_cast<size_t>(nl + ne) * 8 + static_cast<size_t>(nl + ne) * 8 +
+         (static_cast<size_t>(nl) * 2 + static_cast<size_t>(ne) * 2 + k) * 4 + 16;
+}
+
+// smem (optional): the fused kernel's dynamic region.  With it (a.smem_ok)
+// the static lookup arrays are staged up front and the unwind and re-sum
+// touch global memory only for the argmin and cost-table values.
+template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a, unsigned char *smem) {
   using A = typename Acc<T>::type;
   const bool stamp = a.trace && threadIdx.x == 0;
   if (stamp) a.trace[0] = trace_ns();
-  __shared__ A sv[kFinishThreads];
-  __shared__ int64_t si[kFinishThreads];
+  const bool sm = a.smem_ok && smem;
+  double *terms = sm ? reinterpret_cast<double *>(smem) : a.terms;
+  const int64_t *cat_off = a.cat_off, *xoff = a.xoff;
+  int32_t *idx = a.indices;
+  const int32_t *counts = a.counts, *esrc = a.esrc, *edst = a.edst;
+  int32_t *ncount = nullptr;
+  if (sm) { // stage the lookup arrays (independent loads, all in flight at once)
+    int64_t *co = reinterpret_cast<int64_t *>(terms + a.nl + a.ne), *xo = co + a.nl;
+    int32_t *ix = reinterpret_cast<int32_t *>(xo + a.ne), *cn = ix + a.nl, *es = cn + a.nl, *ed = es + a.ne;
+    ncount = ed + a.ne;
+    for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) co[l] = a.cat_off[l], cn[l] = a.counts[l];
+    for (int e = threadIdx.x; e < a.ne; e += kFinishThreads) xo[e] = a.xoff[e], es[e] = a.esrc[e], ed[e] = a.edst[e];
+    for (int d = threadIdx.x; d < a.k; d += kFinishThreads) ncount[d] = a.nodes[d].count;
+    cat_off = co, xoff = xo, idx = ix, counts = cn, esrc = es, edst = ed;
+  }
+  __shared__ A sv[kFinishThreads / 32];
+  __shared__ int64_t si[kFinishThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const A *bv = static_cast<const A *>(a.blk_val);
   A best = A(0);
   int64_t bi = INT64_MAX;
-  for (int b = threadIdx.x; b < a.nblk; b += kFinishThreads) {
-    const int64_t oi = a.blk_idx[b];
-    if (oi == INT64_MAX) continue;
-    const A ov = bv[b];
-    if (bi == INT64_MAX || ov < best || (ov == best && oi < bi)) best = ov, bi = oi;
-  }
-  sv[threadIdx.x] = best;
-  si[threadIdx.x] = bi;
+  if (stamp) a.trace[5] = trace_ns();
+  for (int b = threadIdx.x; b < a.nblk; b += kFinishThreads) keep_best<A>(bv[b], a.blk_idx[b], best, bi);
+  if (stamp) a.trace[6] = trace_ns();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) keep_best<A>(shfl_xor_any<A>(best, o), __shfl_xor_sync(0xffffffffu, bi, o), best, bi);
+  if (lane == 0) sv[warp] = best, si[warp] = bi;
   __syncthreads();
-  for (int s = kFinishThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const A ov = sv[threadIdx.x + s];
-      const int64_t oi = si[threadIdx.x + s];
-      if (oi != INT64_MAX &&
-          (si[threadIdx.x] == INT64_MAX || ov < sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])))
-        sv[threadIdx.x] = ov, si[threadIdx.x] = oi;
+  if (stamp) a.trace[7] = trace_ns();
+  if (warp == 0) {
+    best = lane < kFinishThreads / 32 ? sv[lane] : A(0);
+    bi = lane < kFinishThreads / 32 ? si[lane] : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) keep_best<A>(shfl_xor_any<A>(best, o), __shfl_xor_sync(0xffffffffu, bi, o), best, bi);
+    if (lane == 0) {
+      int64_t r = bi;
+      for (int d = a.k - 1; d >= 0; --d) {
+        const int32_t cnt = ncount ? ncount[d] : a.nodes[d].count;
+        a.digits[d] = static_cast<int32_t>(r % cnt);
+        r /= cnt;
+      }
+      *a.final_cost = ldexp(static_cast<double>(best), -a.shift);
     }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int64_t r = si[0];
-    for (int d = a.k - 1; d >= 0; --d) {
-      a.digits[d] = static_cast<int32_t>(r % a.nodes[d].count);
-      r /= a.nodes[d].count;
-    }
-    *a.final_cost = ldexp(static_cast<double>(sv[0]), -a.shift);
   }
   if (stamp) a.trace[1] = trace_ns();
   if (a.n_rec < 0) return;
+  for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) idx[l] = -1;
   __syncthreads();
-  for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) a.indices[l] = -1;
+  for (int d = threadIdx.x; d < a.k; d += kFinishThreads) idx[a.node_layer[d]] = a.digits[d];
+  // waves, last first; each thread's record of the next group is fetched
+  // before the barrier that ends the current one
+  UnwindRec u{};
+  bool have = false;
+  if (a.n_groups > 0) {
+    const int q = a.group_begin[0] + threadIdx.x;
+    have = q < a.group_begin[1];
+    if (have) u = a.recs[q];
+  }
   __syncthreads();
-  for (int d = threadIdx.x; d < a.k; d += kFinishThreads) a.indices[a.node_layer[d]] = a.digits[d];
-  __syncthreads();
-  for (int gidx = 0; gidx < a.n_groups; ++gidx) { // waves, last first
+  for (int gidx = 0; gidx < a.n_groups; ++gidx) {
     for (int q = a.group_begin[gidx] + threadIdx.x; q < a.group_begin[gidx + 1]; q += kFinishThreads) {
-      const UnwindRec u = a.recs[q];
-      const int64_t at = static_cast<int64_t>(a.indices[u.src]) * u.cols + a.indices[u.dst];
-      if (u.n == 0) {
-        a.indices[u.removed] = u.am[at];
+      const UnwindRec r = q == a.group_begin[gidx] + static_cast<int>(threadIdx.x) && have ? u : a.recs[q];
+      const int64_t at = static_cast<int64_t>(idx[r.src]) * r.cols + idx[r.dst];
+      if (r.n == 0) {
+        idx[r.removed] = r.am[at];
       } else {
-        const uint16_t *pth = u.am + at * u.n;
-        for (int k = 0; k < u.n; ++k) a.indices[a.chain_nodes[u.removed + k]] = pth[k];
+        const uint16_t *pth = r.am + at * r.n;
+        for (int k = 0; k < r.n; ++k) idx[a.chain_nodes[r.removed + k]] = pth[k];
       }
+    }
+    have = false;
+    if (gidx + 1 < a.n_groups) {
+      const int q = a.group_begin[gidx + 1] + threadIdx.x;
+      have = q < a.group_begin[gidx + 2];
+      if (have) u = a.recs[q];
     }
     __syncthreads();
   }
   if (stamp) a.trace[2] = trace_ns();
   const T *onode = static_cast<const T *>(a.onode);
   const T *oxfer = static_cast<const T *>(a.oxfer);
-  for (int l = threadIdx.x; l < a.nl; l += kFinishThreads)
-    a.terms[l] = ldexp(static_cast<double>(onode[a.cat_off[l] + a.indices[l]]), -a.shift);
+  for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) {
+    terms[l] = ldexp(static_cast<double>(onode[cat_off[l] + idx[l]]), -a.shift);
+    if (idx != a.indices) a.indices[l] = idx[l];
+  }
   for (int e = threadIdx.x; e < a.ne; e += kFinishThreads)
-    a.terms[a.nl + e] = ldexp(
-        static_cast<double>(oxfer[a.xoff[e] + static_cast<int64_t>(a.indices[a.esrc[e]]) * a.counts[a.edst[e]] +
-                                  a.indices[a.edst[e]]]),
-        -a.shift);
+    terms[a.nl + e] = ldexp(
+        static_cast<double>(oxfer[xoff[e] + static_cast<int64_t>(idx[esrc[e]]) * counts[edst[e]] + idx[edst[e]]]), -a.shift);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) { // the reference's order: nodes by layer, then edges by id
     double t = 0.0;
-    for (int x = 0; x < a.nl + a.ne; ++x) t += a.terms[x];
+    for (int x = 0; x < a.nl + a.ne; ++x) t += terms[x];
     *a.cost = t;
   }
   if (stamp) a.trace[3] = trace_ns();

@@ -83,9 +83,10 @@ struct pp_prepared {
   Tables *t = nullptr;
   std::unique_ptr<Tables> own_t;
   bool transient = true;
-  DBuf<unsigned char> dmem;
+  DBuf<unsigned char> dmem, dscratch;
   PinnedBuf hmem;
   unsigned char *dbase = nullptr, *hbase = nullptr;
+  unsigned char *sbase = nullptr; // device-only scratch (kernel-written buffers)
   size_t image_off = 0, image_bytes = 0, res_off = 0, res_bytes = 0, off_idx = 0, off_cost = 0;
   std::vector<std::function<void(cudaStream_t)>> steps;
   int launches_per_run = 0;
@@ -99,6 +100,7 @@ struct pp_prepared {
   int n_stamps = 0;
   size_t trace_off = 0; // PARPLAN_WAVE_TRACE: 8 stamps per wave (printed by pp_plan_profile)
   std::vector<char> phase_chain; // fused phases that are chain segments (profile kind 16)
+  int nblk_dbg = 0;
   std::vector<double> fused_wave_work;
 
   ~pp_prepared() {
@@ -109,8 +111,31 @@ struct pp_prepared {
 
 namespace pp {
 
+// PARPLAN_TRACE=2: host-side timing of build_steps' stages
+struct StageClock {
+  bool on = false;
+  std::vector<std::pair<const char *, std::chrono::steady_clock::time_point>> marks;
+  StageClock() {
+    const char *e = std::getenv("PARPLAN_TRACE");
+    on = e && std::atoi(e) >= 2;
+    if (on) marks.emplace_back("start", std::chrono::steady_clock::now());
+  }
+  void mark(const char *name) {
+    if (on) marks.emplace_back(name, std::chrono::steady_clock::now());
+  }
+  ~StageClock() {
+    if (!on) return;
+    std::fprintf(stderr, "[parplan] build_steps:");
+    for (size_t k = 1; k < marks.size(); ++k)
+      std::fprintf(stderr, " %s %.1f", marks[k].first,
+                   std::chrono::duration<double, std::micro>(marks[k].second - marks[k - 1].second).count());
+    std::fprintf(stderr, " us\n");
+  }
+};
+
 template <class T>
 static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
+  StageClock clk;
   pp_context *ctx = P->ctx;
   Graph &g = *P->g;
   Tables &t = *P->t;
@@ -319,7 +344,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<WaveRange> waves;
     std::vector<std::tuple<const void *, void *, size_t>> final_gathers; // sharded: final edges + argmins
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
-    size_t oG, oT, oFW, oST, oTR, oCN;
+    size_t oG, oT, oFW, oST, oTR, oCN; // oT, oST, oTR (+1), oBV, oBI: scratch offsets
+    size_t scratch = 0;                // bytes of the scratch section
     int n_phases = 0;                // fused kernel: waves / chain segments
     size_t dyn_smem = 0;             // fused kernel dynamic shared memory
     std::vector<char> phase_chain;   // phase is a chain segment
@@ -334,8 +360,16 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   const int fused_nc = use_fused ? std::max(1, env_int("PARPLAN_CLUSTER", 1)) : 1;
   const int64_t narrow_items = use_fused ? env_int("PARPLAN_NARROW_ITEMS", 0) : 0;
   const size_t kChainSmemMax = static_cast<size_t>(env_int("PARPLAN_CHAIN_SMEM_KB", 110)) * 1024;
-  auto make_image = [&](unsigned char *db) {
+  // sb: base of the device-only scratch section (buffers the kernels write:
+  // enumeration block results, cost terms, stamps, chain path tables), not uploaded
+  auto make_image = [&](unsigned char *db, unsigned char *sb) {
     Image im;
+    im.pk.bytes.reserve(ctx->last_image_bytes + 4096);
+    auto scr = [&](size_t bytes) {
+      const size_t off = im.scratch;
+      im.scratch = off + align256(bytes);
+      return off;
+    };
     auto tabp = [&](int id) -> const T * {
       if (id < t.ne) {
         const T *ox = bp ? reinterpret_cast<const T *>(db + off_tables + 3 * align256(static_cast<size_t>(t.ncells) * 8))
@@ -562,8 +596,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             sg.items += (cd.nu + rows - 1) / rows;
             if (path && m.size() >= 3) { // path table inside the image (rewritten by every run)
               const FoldDesc<T> &fl = folds[m.back()];
-              const size_t off = im.pk.put(std::vector<uint16_t>(static_cast<size_t>(cd.nu) * fl.nv * m.size()));
-              cd.path = reinterpret_cast<uint16_t *>(db + off_image + off);
+              const size_t off = scr(static_cast<size_t>(cd.nu) * fl.nv * m.size() * sizeof(uint16_t));
+              cd.path = reinterpret_cast<uint16_t *>(sb + off);
               ChainRec cr{static_cast<int>(chain_nodes.size()), static_cast<int>(m.size()), cd.path};
               for (size_t q : m) chain_nodes.push_back(s.ops[static_cast<size_t>(fold_ops[q].oi)].removed);
               for (size_t q : m) chain_of_op[static_cast<size_t>(fold_ops[q].oi)] = static_cast<int>(chain_recs.size());
@@ -640,7 +674,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     Packer &pk = im.pk;
     im.oG = pk.put(groups);
     im.nG = static_cast<int>(groups.size()) - 1;
-    im.oT = pk.put(std::vector<double>(static_cast<size_t>(t.nl + t.ne)));
+    im.oT = scr(static_cast<size_t>(t.nl + t.ne) * sizeof(double));
     im.oMP = pk.put(mpf);
     im.oF = pk.put(folds);
     im.oM = pk.put(merges);
@@ -685,8 +719,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       for (const Segment &S : segs) im.dyn_smem = std::max(im.dyn_smem, S.smem);
       im.phase_chain.clear();
       for (const auto &e : fw) im.phase_chain.push_back(e.n_chains > 0);
-      im.oST = pk.put(std::vector<uint64_t>(fw.size() + 4));
-      im.oTR = env_int("PARPLAN_WAVE_TRACE", 0) ? pk.put(std::vector<uint64_t>(16 * fw.size() + 16)) : 0;
+      im.oST = scr((fw.size() + 4) * sizeof(uint64_t));
+      im.oTR = env_int("PARPLAN_WAVE_TRACE", 0) ? scr((16 * fw.size() + 16) * sizeof(uint64_t)) + 1 : 0; // +1: nonzero flag
     }
     im.oN = pk.put(en);
     im.oE = pk.put(ee);
@@ -705,8 +739,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       im.oRat = pk.put(bp->rates);
       im.oBw = pk.put(bp->bw);
     }
-    im.oBV = pk.put(std::vector<A>(static_cast<size_t>(nblk)));
-    im.oBI = pk.put(std::vector<int64_t>(static_cast<size_t>(nblk)));
+    im.oBV = scr(static_cast<size_t>(nblk) * sizeof(A));
+    im.oBI = scr(static_cast<size_t>(nblk) * sizeof(int64_t));
     // result slots, contiguous: indices[nl] | digits[K] | final_cost | cost
     im.oRes = pk.put(std::vector<int32_t>(static_cast<size_t>(t.nl) + static_cast<size_t>(K) + 2));
     im.oIdx = im.oRes;
@@ -715,29 +749,37 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     return im;
   };
 
+  clk.mark("memplan");
   // sizes (pointer values do not change the layout)
   // The image holds absolute device pointers, so it is built against the final
   // base.  One-shot plans reuse the context pool: build against the current
   // pool and rebuild only when the pool has to grow (first calls).
   Image im;
   if (P->transient) {
-    im = make_image(ctx->plan_pool.p);
+    im = make_image(ctx->plan_pool.p, ctx->plan_scratch.p);
     const size_t total = off_image + align256(im.pk.size());
-    if (total > ctx->plan_pool.n || !ctx->plan_pool.p) {
+    if (total > ctx->plan_pool.n || !ctx->plan_pool.p || im.scratch > ctx->plan_scratch.n || !ctx->plan_scratch.p) {
       ctx->plan_pool.ensure(total + total / 4);
-      im = make_image(ctx->plan_pool.p);
+      ctx->plan_scratch.ensure(std::max<size_t>(im.scratch + im.scratch / 4, 256));
+      im = make_image(ctx->plan_pool.p, ctx->plan_scratch.p);
     }
     P->dbase = ctx->plan_pool.p;
+    P->sbase = ctx->plan_scratch.p;
     P->hbase = static_cast<unsigned char *>(ctx->plan_pinned.ensure(align256(im.pk.size())));
+    clk.mark("image");
   } else {
-    const size_t total = off_image + align256(make_image(nullptr).pk.size());
+    const Image sizing = make_image(nullptr, nullptr);
+    const size_t total = off_image + align256(sizing.pk.size());
     P->dmem.alloc(total);
+    P->dscratch.alloc(std::max<size_t>(sizing.scratch, 256));
     P->dbase = P->dmem.p;
+    P->sbase = P->dscratch.p;
     // poison: a slot the device work fails to write shows up as garbage
     PP_CUDA(cudaMemsetAsync(P->dbase, 0xFF, total, ctx->stream));
-    im = make_image(P->dbase);
+    im = make_image(P->dbase, P->sbase);
     P->hbase = static_cast<unsigned char *>(P->hmem.ensure(align256(im.pk.size())));
   }
+  ctx->last_image_bytes = std::max(ctx->last_image_bytes, im.pk.size());
   unsigned char *db = P->dbase;
   unsigned char *dimg = db + off_image;
   std::memcpy(P->hbase, im.pk.bytes.data(), im.pk.size());
@@ -859,8 +901,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     const EnumNode *en = reinterpret_cast<const EnumNode *>(dimg + im.oN);
     const EnumEdge *ee = reinterpret_cast<const EnumEdge *>(dimg + im.oE);
     const int m = static_cast<int>(s.final_edges.size());
-    A *bv = reinterpret_cast<A *>(dimg + im.oBV);
-    int64_t *bi = reinterpret_cast<int64_t *>(dimg + im.oBI);
+    A *bv = reinterpret_cast<A *>(P->sbase + im.oBV);
+    int64_t *bi = reinterpret_cast<int64_t *>(P->sbase + im.oBI);
     if (!use_fused) {
       P->steps.push_back([ctx, en, K, ee, m, space, per_thread, bv, bi, nblk](cudaStream_t st) {
         enum_kernel<T><<<nblk, kEnumThreads, 0, st>>>(en, K, ee, m, space, per_thread, bv, bi);
@@ -873,6 +915,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.blk_val = bv;
     fa.blk_idx = bi;
     fa.nblk = nblk;
+    P->nblk_dbg = nblk;
     fa.nodes = en;
     fa.k = K;
     fa.node_layer = reinterpret_cast<const int32_t *>(dimg + im.oL);
@@ -886,7 +929,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.n_rec = static_cast<int>(s.node_ops);
     fa.group_begin = reinterpret_cast<const int32_t *>(dimg + im.oG);
     fa.n_groups = im.nG;
-    fa.terms = reinterpret_cast<double *>(dimg + im.oT);
+    fa.terms = reinterpret_cast<double *>(P->sbase + im.oT);
     fa.nl = t.nl;
     fa.onode = bp ? static_cast<const void *>(t.node.p)
                   : (t.mode == kFP64 ? static_cast<const void *>(t.node.p) : static_cast<const void *>(t.node32.p));
@@ -920,15 +963,17 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       fz.space = space, fz.per_thread = per_thread;
       fz.blk_val = bv, fz.blk_idx = bi, fz.nblk = nblk;
       fz.fin = fa;
-      fz.stamps = reinterpret_cast<uint64_t *>(dimg + im.oST);
+      fz.stamps = reinterpret_cast<uint64_t *>(P->sbase + im.oST);
       fz.stage = env_int("PARPLAN_STAGE", 1);
-      fz.trace = im.oTR ? reinterpret_cast<uint64_t *>(dimg + im.oTR) : nullptr;
+      fz.trace = im.oTR ? reinterpret_cast<uint64_t *>(P->sbase + im.oTR - 1) : nullptr;
       if (fz.trace) fz.fin.trace = fz.trace + 16 * im.n_phases;
+      fz.fin.smem_ok = finish_smem_bytes(t.nl, t.ne, K) <= im.dyn_smem;
       P->trace_off = im.oTR;
       P->stamp_off = im.oST;
       P->n_stamps = im.n_phases + 4; // start, tables, waves / segments..., enum, finish
       P->fused_wave_work = im.phase_work;
       P->phase_chain = im.phase_chain;
+      clk.mark("steps");
       const size_t dyn = im.dyn_smem;
       {
         // grow the dynamic allowance monotonically; keep the shared-memory
@@ -978,6 +1023,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         PP_REQUIRE(clusters > 0, "fused plan kernel: no co-resident cluster of " + std::to_string(nc));
         cap = std::min<int64_t>(cap, int64_t(clusters) * nc) / nc * nc;
       }
+      clk.mark("occupancy");
       const int64_t want = (items + nc - 1) / nc * nc;
       const unsigned grid = static_cast<unsigned>(std::max<int64_t>(nc, std::min<int64_t>(want, cap)));
       fz.nc = nc;
@@ -1013,6 +1059,8 @@ static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
     bp.bw.assign(dev->bandwidth, dev->bandwidth + static_cast<size_t>(dev->count) * dev->count);
   }
   PP_REQUIRE(P->t->nl == P->g->nl && P->t->ne == P->g->ne, "tables do not match the graph");
+  if (std::getenv("PARPLAN_TRACE") && std::atoi(std::getenv("PARPLAN_TRACE")) >= 2)
+    std::fprintf(stderr, "[parplan] plan_build done\n");
   if (P->t->mode == kFP64)
     build_steps<double>(P, dev ? &bp : nullptr, k_bound);
   else
@@ -1181,11 +1229,11 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
       const int kind = P->step_kind[static_cast<size_t>(k)];
       if (kind == 10 && P->n_stamps > 1) { // fused kernel: expand its phases (globaltimer stamps)
         std::vector<uint64_t> st(static_cast<size_t>(P->n_stamps));
-        PP_CUDA(cudaMemcpy(st.data(), P->dbase + P->image_off + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
+        PP_CUDA(cudaMemcpy(st.data(), P->sbase + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
         const int waves = P->n_stamps - 4;
         if (P->trace_off) {
           std::vector<uint64_t> tr(static_cast<size_t>(16 * waves + 16));
-          PP_CUDA(cudaMemcpy(tr.data(), P->dbase + P->image_off + P->trace_off, tr.size() * 8, cudaMemcpyDeviceToHost));
+          PP_CUDA(cudaMemcpy(tr.data(), P->sbase + P->trace_off - 1, tr.size() * 8, cudaMemcpyDeviceToHost));
           for (int w = 0; w < waves; ++w) {
             const uint64_t *r = &tr[static_cast<size_t>(16 * w)];
             const uint64_t b0 = st[static_cast<size_t>(w) + 1]; // block 0 left the previous barrier
@@ -1196,9 +1244,11 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
                          w, rel(r[0]), rel(r[7]), rel(r[1]), rel(r[5]), rel(r[6]), rel(r[2]), rel(r[3]), rel(r[4]));
           }
           const uint64_t *fr = &tr[static_cast<size_t>(16 * waves)];
-          std::fprintf(stderr, "finish: reduce %.0f unwind %.0f resum %.0f results %.0f ns\n",
+          std::fprintf(stderr, "finish: reduce %.0f unwind %.0f resum %.0f results %.0f ns (stage %.0f blk %.0f sync %.0f; nblk %d)\n",
                        static_cast<double>(fr[1] - fr[0]), static_cast<double>(fr[2] - fr[1]),
-                       static_cast<double>(fr[3] - fr[2]), static_cast<double>(fr[4] - fr[3]));
+                       static_cast<double>(fr[3] - fr[2]), static_cast<double>(fr[4] - fr[3]),
+                       static_cast<double>(fr[5] - fr[0]), static_cast<double>(fr[6] - fr[5]),
+                       static_cast<double>(fr[7] - fr[6]), P->nblk_dbg);
         }
         for (int ph = 0; ph + 1 < P->n_stamps; ++ph) {
           const int pk = ph == 0       ? 11

@@ -1,5 +1,5 @@
 import os, sys, time
-os.environ["PARPLAN_TRACE"] = "1"
+os.environ.setdefault("PARPLAN_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1802_04924_b200 as P
 ctx = P.Context(0)
