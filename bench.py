@@ -293,6 +293,27 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def committed_traffic(kernel):
+    """DRAM bytes (read + write) of one launch of `kernel` from the committed
+    ncu --set full summary under profiles/ (the roofline's traffic field)."""
+    import csv
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_full_summary.csv")),
+                       reverse=True):
+        with open(path) as f:
+            rows = [r for r in csv.DictReader(f) if kernel in r["kernel"]]
+        if not rows:
+            continue
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        total = 0.0
+        for r in rows:
+            if r["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                total += float(r["value"]) * scale.get(r["unit"], 1.0)
+        return total, f"{os.path.basename(path)}: dram__bytes_read.sum + dram__bytes_write.sum of one captured launch"
+    return None, "no committed ncu --set full summary"
+
+
 def minplus(P, ctx, args, flush, stream):
     """Config-5 synthetic sweep point: 1000 layers (bp 0.3, seed 1 topology),
     C configs per layer, device-generated dyadic tables, exact int32 DP."""
@@ -341,9 +362,10 @@ def minplus(P, ctx, args, flush, stream):
     sms = 148
     peak_tflops = sms * 128 * 2 * f_mhz * 1e6 / 1e12  # FP32 CUDA-core: 2 ops (add + min) per cell at 1 cell/lane/clk
     achieved = 2.0 * cells / (wave_ms * 1e-3) / 1e12
+    traffic, traffic_basis = committed_traffic("mp_fold_kernel")
     return {
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tflops, "traffic": None,
+                     "frac": achieved / peak_tflops, "traffic": traffic, "traffic_basis": traffic_basis,
                      "kernel": "mp_fold_kernel (K3 Eq. 2 fold, VIADDMNMX.S16x2), config-5 graph",
                      "launches": len(folds) // len(runs),
                      "peak_basis": f"148 SM x 128 FP32 lanes x 2 ops x {f_mhz:.0f} MHz (measured SM clock under load)"},
