@@ -101,6 +101,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
   const bool stamp = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
   int ph = 0;
   if (stamp) a.stamps[ph++] = global_ns();
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + 2048 + blockIdx.x] = global_ns();
   if (a.has_build) {
     const BuildArgs &B = a.build;
     const int64_t n = B.ncells + a.xcells;
@@ -126,7 +127,12 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
       }
       xfer_cells_warp(B, edge, x);
     }
+    if (a.trace) { // per-block end of the build loop (profiling)
+      __syncthreads();
+      if (threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + blockIdx.x] = global_ns();
+    }
     grid.sync();
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + 4096 + blockIdx.x] = global_ns();
   }
   if (stamp) a.stamps[ph++] = global_ns();
   // this block's first item of each wave is staged one wave early: its

@@ -25,11 +25,21 @@
 #include <map>
 
 namespace pp {
-// tuning knobs read per prepare (A/B experiments in one process)
+// tuning knobs read once per prepare (A/B experiments in one process)
 static int env_int(const char *name, int dflt) {
   const char *v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
 }
+struct Knobs {
+  int cluster, narrow_items, chain_smem_kb, panel, panel_side, chains, chain_path, rotate, wave_trace, stage, blocks_per_sm;
+  Knobs()
+      : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
+        chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), panel(env_int("PARPLAN_PANEL", 1)),
+        panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
+        chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
+        wave_trace(env_int("PARPLAN_WAVE_TRACE", 0)), stage(env_int("PARPLAN_STAGE", 1)),
+        blocks_per_sm(env_int("PARPLAN_FUSED_BLOCKS_PER_SM", 0)) {}
+};
 }
 
 namespace pp {
@@ -136,6 +146,7 @@ struct StageClock {
 template <class T>
 static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   StageClock clk;
+  const Knobs kn;
   pp_context *ctx = P->ctx;
   Graph &g = *P->g;
   Tables &t = *P->t;
@@ -357,9 +368,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // fused kernel: waves with at most kNarrowItems work items run on the first
   // thread-block cluster alone, with cluster barriers between consecutive
   // narrow waves instead of grid-wide ones
-  const int fused_nc = use_fused ? std::max(1, env_int("PARPLAN_CLUSTER", 1)) : 1;
-  const int64_t narrow_items = use_fused ? env_int("PARPLAN_NARROW_ITEMS", 0) : 0;
-  const size_t kChainSmemMax = static_cast<size_t>(env_int("PARPLAN_CHAIN_SMEM_KB", 110)) * 1024;
+  const int fused_nc = use_fused ? std::max(1, kn.cluster) : 1;
+  const int64_t narrow_items = use_fused ? kn.narrow_items : 0;
+  const size_t kChainSmemMax = static_cast<size_t>(kn.chain_smem_kb) * 1024;
   // sb: base of the device-only scratch section (buffers the kernels write:
   // enumeration block results, cost terms, stamps, chain path tables), not uploaded
   auto make_image = [&](unsigned char *db, unsigned char *sb) {
@@ -412,8 +423,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       // panel tiles: the smallest side whose tile count still fits one round
       // of co-resident blocks (more j-split groups, shorter scans)
       int panel_mode = kPanel16;
-      if (small_wave && env_int("PARPLAN_PANEL", 1)) {
-        const int forced = env_int("PARPLAN_PANEL_SIDE", 0);
+      if (small_wave && kn.panel) {
+        const int forced = kn.panel_side;
         for (int mode : {kPanel4, kPanel8}) {
           const int R = panel_side(mode);
           int64_t n = 0;
@@ -486,7 +497,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           f.nu = nu_eff(op.e1);
           f.nw = t.counts[static_cast<size_t>(op.removed)];
           f.nv = cols[static_cast<size_t>(op.e2)];
-          f.small = small_wave ? (f.nw <= kPanel && env_int("PARPLAN_PANEL", 1) ? panel_mode : 1) : 0;
+          f.small = small_wave ? (f.nw <= kPanel && kn.panel ? panel_mode : 1) : 0;
           const int ts = f.small >= kPanel16 ? panel_side(f.small) : f.small ? kSmallTile : kTile;
           f.late = 0; // set below, once the narrow waves are known
           fold_ops.push_back({op.e1, op.e2, op.ne, w, oi});
@@ -538,7 +549,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<int> chain_last_op;
     std::vector<int32_t> chain_nodes;
     std::vector<int> chain_of_op(s.ops.size(), -1);
-    if (use_fused && env_int("PARPLAN_CHAINS", 1)) {
+    if (use_fused && kn.chains) {
       auto fits = [&](int w, int ws) {
         const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
         if (wr.nm || wr.nf == 0) return false;
@@ -584,7 +595,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           const int64_t cap = 2 * int64_t(ctx->sms);
           int rows = static_cast<int>(std::clamp<int64_t>((rows_total + cap - 1) / cap, 1, kChainRows));
           // unwind path tables for chains of >= 3 folds, when the argmins fit in shared memory
-          bool path = max_len >= 3 && env_int("PARPLAN_CHAIN_PATH", 1);
+          bool path = max_len >= 3 && kn.chain_path;
           while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage, path) > kChainSmemMax) --rows;
           if (path && chain_smem_bytes<T>(rows, max_len, stage, path) > kChainSmemMax) path = false;
           sg.smem = chain_smem_bytes<T>(rows, max_len, stage, path);
@@ -710,7 +721,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         e.narrow = narrow[static_cast<size_t>(w)];
         fw.push_back(e);
         im.phase_work.push_back(wr.cells);
-        if (env_int("PARPLAN_ROTATE", 1)) rot += items;
+        if (kn.rotate) rot += items;
         ++w;
       }
       im.oFW = pk.put(fw);
@@ -720,7 +731,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       im.phase_chain.clear();
       for (const auto &e : fw) im.phase_chain.push_back(e.n_chains > 0);
       im.oST = scr((fw.size() + 4) * sizeof(uint64_t));
-      im.oTR = env_int("PARPLAN_WAVE_TRACE", 0) ? scr((16 * fw.size() + 16) * sizeof(uint64_t)) + 1 : 0; // +1: nonzero flag
+      im.oTR = kn.wave_trace ? scr((16 * fw.size() + 16 + 6400) * sizeof(uint64_t)) + 1 : 0; // +1: nonzero flag
     }
     im.oN = pk.put(en);
     im.oE = pk.put(ee);
@@ -735,7 +746,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     if (bp) {
       im.oLay = pk.put(bp->L);
       im.oEdg = pk.put(bp->E);
-      im.oCfg = pk.put(bp->cfg32);
+      im.oCfg = pk.put(*bp->cfg32);
       im.oRat = pk.put(bp->rates);
       im.oBw = pk.put(bp->bw);
     }
@@ -831,6 +842,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ba.nl = t.nl, ba.ne = t.ne, ba.D = bp->D;
     ba.node_blocks = static_cast<int32_t>(bp->node_blocks);
     ba.bw_uniform = bp->bw_uniform;
+    ba.dbg_no_store = kn.stage == 6;
   }
   if (bp && bp->grid > 0 && !use_fused) {
     const BuildArgs a = ba;
@@ -964,7 +976,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       fz.blk_val = bv, fz.blk_idx = bi, fz.nblk = nblk;
       fz.fin = fa;
       fz.stamps = reinterpret_cast<uint64_t *>(P->sbase + im.oST);
-      fz.stage = env_int("PARPLAN_STAGE", 1);
+      fz.stage = kn.stage;
       fz.trace = im.oTR ? reinterpret_cast<uint64_t *>(P->sbase + im.oTR - 1) : nullptr;
       if (fz.trace) fz.fin.trace = fz.trace + 16 * im.n_phases;
       fz.fin.smem_ok = finish_smem_bytes(t.nl, t.ne, K) <= im.dyn_smem;
@@ -996,7 +1008,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       int64_t items = std::max<int64_t>(nblk, 1);
       if (bp) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
       for (const auto &wr : im.waves) items = std::max<int64_t>(items, wr.ftiles + wr.mblocks);
-      const int per_sm_env = env_int("PARPLAN_FUSED_BLOCKS_PER_SM", 0);
+      const int per_sm_env = kn.blocks_per_sm;
       const int per_sm = per_sm_env > 0 ? std::min(per_sm_env, occ) : occ;
       // cooperative + cluster launch: the grid is whole clusters, all co-resident
       const int nc = fused_nc;
@@ -1054,7 +1066,7 @@ static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
     P->own_t = std::make_unique<Tables>();
     P->t = P->own_t.get();
     P->t->ctx = P->ctx;
-    bp = plan_build(*P->t, *P->g, dev);
+    bp = plan_build(*P->t, *P->g, dev, /*host_configs=*/false);
     bp.rates.assign(dev->compute_rates, dev->compute_rates + dev->count);
     bp.bw.assign(dev->bandwidth, dev->bandwidth + static_cast<size_t>(dev->count) * dev->count);
   }
@@ -1232,7 +1244,7 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
         PP_CUDA(cudaMemcpy(st.data(), P->sbase + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
         const int waves = P->n_stamps - 4;
         if (P->trace_off) {
-          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves + 16));
+          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves + 16 + 6400));
           PP_CUDA(cudaMemcpy(tr.data(), P->sbase + P->trace_off - 1, tr.size() * 8, cudaMemcpyDeviceToHost));
           for (int w = 0; w < waves; ++w) {
             const uint64_t *r = &tr[static_cast<size_t>(16 * w)];
@@ -1242,6 +1254,27 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
                          "wave %2d worker start %6.0f tile %6.0f loaded %6.0f scanned %6.0f merged %6.0f stored %6.0f "
                          "arrive %6.0f leave %6.0f ns\n",
                          w, rel(r[0]), rel(r[7]), rel(r[1]), rel(r[5]), rel(r[6]), rel(r[2]), rel(r[3]), rel(r[4]));
+          }
+          {
+            std::vector<double> be, bs, bx;
+            for (int b = 0; b < 2048; ++b) {
+              const uint64_t x = tr[static_cast<size_t>(16 * waves + 16 + b)];
+              const uint64_t y = tr[static_cast<size_t>(16 * waves + 16 + 2048 + b)];
+              const uint64_t z = tr[static_cast<size_t>(16 * waves + 16 + 4096 + b)];
+              if (x && y && z) be.push_back(static_cast<double>(static_cast<int64_t>(x - st[0]))),
+                  bs.push_back(static_cast<double>(static_cast<int64_t>(y - st[0]))),
+                  bx.push_back(static_cast<double>(static_cast<int64_t>(z - st[0])));
+            }
+            if (!be.empty()) {
+              std::sort(be.begin(), be.end());
+              std::sort(bs.begin(), bs.end());
+              std::sort(bx.begin(), bx.end());
+              std::fprintf(stderr,
+                           "build: %zu blocks start min %.0f max %.0f; arrive min %.0f median %.0f p90 %.0f max %.0f; "
+                           "leave min %.0f max %.0f ns (phase %.0f)\n",
+                           be.size(), bs.front(), bs.back(), be.front(), be[be.size() / 2], be[be.size() * 9 / 10], be.back(),
+                           bx.front(), bx.back(), static_cast<double>(st[1] - st[0]));
+            }
           }
           const uint64_t *fr = &tr[static_cast<size_t>(16 * waves)];
           std::fprintf(stderr, "finish: reduce %.0f unwind %.0f resum %.0f results %.0f ns (stage %.0f blk %.0f sync %.0f; nblk %d)\n",

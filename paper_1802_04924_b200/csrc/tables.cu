@@ -325,7 +325,7 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
     t.ctx = ctx;
     const BuildPlan bp = plan_build(t, gh->impl, dev);
     Packer pk;
-    const size_t oL = pk.put(bp.L), oE = pk.put(bp.E), oC = pk.put(bp.cfg32);
+    const size_t oL = pk.put(bp.L), oE = pk.put(bp.E), oC = pk.put(*bp.cfg32);
     const size_t oR = pk.put(dev->compute_rates, static_cast<size_t>(bp.D));
     const size_t oB = pk.put(dev->bandwidth, static_cast<size_t>(bp.D) * bp.D);
     t.node.alloc(static_cast<size_t>(t.ncells));
@@ -361,7 +361,7 @@ void launch_build(pp_context *ctx, cudaStream_t st, const BuildArgs &a, int64_t 
   check_launch(ctx);
 }
 
-BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev) {
+BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev, bool host_configs) {
   const int D = dev->count;
   if (D < 1) throw parplan::InputError("device graph: need at least one device");
   // DeviceGraph validation (graph.hpp:193-214)
@@ -376,13 +376,13 @@ BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev) {
   }
   const Graph::Catalogs &cats = g.catalogs(D); // cached per (graph, D)
   const std::vector<int32_t> &counts = cats.counts;
-  t.configs = cats.configs;
+  if (host_configs) t.configs = cats.configs; // kept for pp_tables_download only
   init_layout(t, g, counts);
   t.mode = kFP64;
   t.analytic = true;
   BuildPlan bp;
   bp.D = D;
-  bp.cfg32 = cats.configs32;
+  bp.cfg32 = &cats.configs32;
 
   double bw_uniform = dev->bandwidth[D > 1 ? 1 : 0];
     for (int p = 0; p < D; ++p)

@@ -71,6 +71,7 @@ struct BuildArgs {
   int32_t nl, ne, D;
   int32_t node_blocks;
   double bw_uniform; // > 0 when every off-diagonal bandwidth is this value
+  int32_t dbg_no_store; // profiling experiment only
 };
 
 struct BuildPlan {
@@ -80,12 +81,12 @@ struct BuildPlan {
   double bw_uniform = 0.0;
   int D = 0;
   std::vector<double> rates, bw; // the device graph, for plans that embed it
-  std::vector<int32_t> cfg32;    // catalogs as the kernels read them
+  const std::vector<int32_t> *cfg32 = nullptr; // catalogs as the kernels read them (the graph's cache)
 };
 
 // Fills t's layout (catalogs, offsets; FP64 analytic mode, no allocation) and
 // the K1/K2 launch descriptors for graph g on devices dev.
-BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev);
+BuildPlan plan_build(Tables &t, const Graph &g, const pp_device_desc *dev, bool host_configs = true);
 void launch_build(pp_context *ctx, cudaStream_t st, const BuildArgs &a, int64_t grid);
 
 // Decides fixed point vs FP64 for host tables and fills the span bounds.
