@@ -287,7 +287,7 @@ __device__ __forceinline__ void xfer_cells_warp(const BuildArgs &a, int edge, in
     if (a.bw_uniform > 0.0) {
       const int64_t mv = xfer_maxvol_separable(c);
       if (mv >= 0)
-        if (!a.dbg_no_store) a.xfer[c.out] = xfer_seconds(a, mv);
+        a.xfer[c.out] = xfer_seconds(a, mv);
       else
         hard = true;
     } else {
@@ -308,7 +308,7 @@ __device__ __forceinline__ void xfer_cells_warp(const BuildArgs &a, int edge, in
       const int64_t other = __shfl_xor_sync(kFull, mv, o);
       mv = other > mv ? other : mv;
     }
-    if (lane == src && !a.dbg_no_store) a.xfer[c.out] = xfer_seconds(a, mv);
+    if (lane == src) a.xfer[c.out] = xfer_seconds(a, mv);
   }
 }
 

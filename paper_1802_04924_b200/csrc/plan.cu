@@ -842,7 +842,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ba.nl = t.nl, ba.ne = t.ne, ba.D = bp->D;
     ba.node_blocks = static_cast<int32_t>(bp->node_blocks);
     ba.bw_uniform = bp->bw_uniform;
-    ba.dbg_no_store = kn.stage == 6;
   }
   if (bp && bp->grid > 0 && !use_fused) {
     const BuildArgs a = ba;

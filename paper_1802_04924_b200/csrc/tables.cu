@@ -334,7 +334,7 @@ pp_status pp_tables_build(pp_context *ctx, const pp_graph *gh, const pp_device_d
     t.xfer64.alloc(static_cast<size_t>(t.xcells));
     ctx->begin();
     unsigned char *base = ctx->upload(pk);
-    BuildArgs a;
+    BuildArgs a{};
     a.layers = reinterpret_cast<const LayerDev *>(base + oL);
     a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
     a.cfg = reinterpret_cast<const int32_t *>(base + oC);

@@ -71,7 +71,6 @@ struct BuildArgs {
   int32_t nl, ne, D;
   int32_t node_blocks;
   double bw_uniform; // > 0 when every off-diagonal bandwidth is this value
-  int32_t dbg_no_store; // profiling experiment only
 };
 
 struct BuildPlan {
