@@ -169,9 +169,10 @@ __device__ __forceinline__ int64_t xfer_maxvol_separable(const XferCell &c) {
   int64_t mmax = 1;
   bool easy = false;
   int dsum = 0, S = 1, D = 1;
+  int bm[4], sm2[4], b2[4]; // per dimension: max best, max second over the maximisers, best non-maximiser
 #pragma unroll
   for (int d = 3; d >= 0; --d) {
-    int bmax = -1, dfirst = 0;
+    int bmax = -1, dfirst = 0, smax = 0, bnext = -1;
     bool nonunique = false, dvar = false;
     for (int x = 0; x < c.cd[d]; ++x) {
       const int olo = x * c.dpiece[d];
@@ -180,20 +181,45 @@ __device__ __forceinline__ int64_t xfer_maxvol_separable(const XferCell &c) {
       const geo::DimStats<int> st = dim_stats_fast(lo, hi, c.spiece[d], c.rcp[d]);
       const int delta = st.arg * S - x * D;
       if (st.best > bmax) {
-        bmax = st.best, nonunique = !st.unique, dvar = false, dfirst = delta;
+        bnext = bmax > bnext ? bmax : bnext;
+        bmax = st.best, nonunique = !st.unique, dvar = false, dfirst = delta, smax = st.second;
       } else if (st.best == bmax) {
         nonunique |= !st.unique;
         dvar |= delta != dfirst;
+        smax = st.second > smax ? st.second : smax;
+      } else {
+        bnext = st.best > bnext ? st.best : bnext;
       }
     }
     mmax *= bmax;
     easy |= nonunique | dvar;
     dsum += dfirst;
+    bm[d] = bmax, sm2[d] = smax, b2[d] = bnext;
     S *= c.cs[d];
     D *= c.cd[d];
   }
   if (mmax == 0) return 0;
   if (easy || dsum != 0) return mmax;
+  // Every maximising q is "diagonal" (its unique best source is q itself), so
+  // over them the answer is the best other source: max_d S_d * prod_{e!=d}
+  // bmax_e (S_d: largest second-best over the maximising digits).  Any other
+  // q has M(q) <= U = max_d b2_d * prod_{e!=d} bmax_e; when U <= that value
+  // (no non-maximising digit at all in the diagonal cells) it is exact.
+  int64_t alt = 0, U = -1;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    int64_t rest = 1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (e != d) rest *= bm[e];
+    const int64_t a = rest * sm2[d];
+    alt = a > alt ? a : alt;
+    if (b2[d] >= 0) {
+      const int64_t u = rest * b2[d];
+      U = u > U ? u : U;
+    }
+  }
+  if (U <= alt) return alt;
   return -1;
 }
 
