@@ -31,10 +31,12 @@ static int env_int(const char *name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 struct Knobs {
-  int cluster, narrow_items, chain_smem_kb, panel, panel_side, chains, chain_path, rotate, wave_trace, stage, blocks_per_sm;
+  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, panel, panel_side, chains, chain_path, rotate,
+      wave_trace, stage, blocks_per_sm;
   Knobs()
       : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
-        chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), panel(env_int("PARPLAN_PANEL", 1)),
+        chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
+        chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), panel(env_int("PARPLAN_PANEL", 1)),
         panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
         chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
         wave_trace(env_int("PARPLAN_WAVE_TRACE", 0)), stage(env_int("PARPLAN_STAGE", 1)),
@@ -550,24 +552,47 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<int32_t> chain_nodes;
     std::vector<int> chain_of_op(s.ops.size(), -1);
     if (use_fused && kn.chains) {
-      auto fits = [&](int w, int ws) {
+      auto fits = [&](int w, int ws, size_t limit) {
         const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
         if (wr.nm || wr.nf == 0) return false;
         for (size_t q = wr.f0; q < wr.f0 + static_cast<size_t>(wr.nf); ++q) {
           const FoldOps &o = fold_ops[q];
           if (folds[q].nw > kChainMax || folds[q].nv > kChainMax) return false;
-          if (chain_smem_bytes<T>(1, 64, chain_stage_bytes<T>(folds[q].nw, folds[q].nv), false) > kChainSmemMax) return false;
+          if (chain_smem_bytes<T>(1, 64, chain_stage_bytes<T>(folds[q].nw, folds[q].nv), false) > limit) return false;
           if (prod_wave[static_cast<size_t>(o.e2)] >= ws) return false;
           const int p1 = prod_wave[static_cast<size_t>(o.e1)];
           if (p1 >= ws && p1 >= w) return false;
         }
         return true;
       };
-      for (int w = 1; w <= nwv;) {
-        int we = w;
-        if (fits(w, w))
-          while (we + 1 <= nwv && fits(we + 1, w)) ++we;
-        if (we > w) {
+      auto ranges = [&](size_t limit) {
+        std::vector<std::pair<int, int>> r;
+        for (int w = 1; w <= nwv;) {
+          int we = w;
+          if (fits(w, w, limit))
+            while (we + 1 <= nwv && fits(we + 1, w, limit)) ++we;
+          if (we > w) r.emplace_back(w, we);
+          w = we + 1;
+        }
+        return r;
+      };
+      auto barriers_saved = [](const std::vector<std::pair<int, int>> &r) {
+        int n = 0;
+        for (const auto &x : r) n += x.second - x.first;
+        return n;
+      };
+      // segments whose staging needs more than kChainSmemMax run the kernel at one
+      // CTA per SM (slower table build, fewer wave CTAs): only worth it when they
+      // remove many more barriers (VGG-16: the whole network is one chain)
+      std::vector<std::pair<int, int>> R = ranges(kChainSmemMax);
+      size_t limit = kChainSmemMax;
+      {
+        const size_t big = static_cast<size_t>(kn.chain_smem_big_kb) * 1024;
+        const auto R2 = ranges(big);
+        if (barriers_saved(R2) - barriers_saved(R) >= kn.chain_big_gain) R = R2, limit = big;
+      }
+      for (const auto &[w, we] : R) {
+        {
           Segment sg{w, we, {}, {}, 0, 0, 0};
           std::vector<int> chain_of_table(static_cast<size_t>(E_total), -1);
           std::vector<std::vector<size_t>> members;
@@ -596,8 +621,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           int rows = static_cast<int>(std::clamp<int64_t>((rows_total + cap - 1) / cap, 1, kChainRows));
           // unwind path tables for chains of >= 3 folds, when the argmins fit in shared memory
           bool path = max_len >= 3 && kn.chain_path;
-          while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage, path) > kChainSmemMax) --rows;
-          if (path && chain_smem_bytes<T>(rows, max_len, stage, path) > kChainSmemMax) path = false;
+          while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage, path) > limit) --rows;
+          if (path && chain_smem_bytes<T>(rows, max_len, stage, path) > limit) path = false;
           sg.smem = chain_smem_bytes<T>(rows, max_len, stage, path);
           sg.stage = stage;
           for (const auto &m : members) {
@@ -620,7 +645,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           for (int x = w; x <= we; ++x) seg_of[static_cast<size_t>(x)] = static_cast<int>(segs.size());
           segs.push_back(std::move(sg));
         }
-        w = we + 1;
       }
     }
     std::vector<char> narrow(static_cast<size_t>(nwv) + 2, 0), gbar(static_cast<size_t>(nwv) + 2, 1);
