@@ -53,6 +53,8 @@ struct MpFold {
   uint16_t *am;  // [nu][nv]
   // scratch
   int32_t *ra, *cb;   // [nu], [nv]
+  int32_t *cbp;       // [col_segs][nv] partial column minima (mp_reduce), folded into cb by mp_pack
+  int32_t col_segs;   // j segments of kMpRedColJ per column block
   uint32_t *A2T;      // [nwp][nup]
   uint16_t *A16;      // [nu][nwp]
   uint16_t *B16;      // [nwp][nvp]
@@ -78,8 +80,10 @@ template <class F> __device__ __forceinline__ int find_desc(const MpFold *d, int
   return lo;
 }
 
-// ---- mp_reduce: ra (one warp per row) and cb (one thread per column) -------
+// ---- mp_reduce: ra (one warp per row) and partial cb (32 columns x one
+// j segment per block: 8 warps x kMpRedColJ / 8 rows each, loads unrolled) --
 constexpr int kMpRedRowsPerBlock = 8; // 8 warps
+constexpr int kMpRedColJ = 128;       // j rows per column block
 __global__ void __launch_bounds__(256) mp_reduce_kernel(const MpFold *folds, int n) {
   const int64_t b = blockIdx.x;
   const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.red_begin; })];
@@ -91,26 +95,49 @@ __global__ void __launch_bounds__(256) mp_reduce_kernel(const MpFold *folds, int
     const int lane = threadIdx.x & 31;
     int m = INT_MAX;
     const int32_t *row = f.t1 + static_cast<int64_t>(i) * f.nw;
-    for (int j = lane; j < f.nw; j += 32) m = min(m, f.w[j] + row[j]);
+    int j = lane;
+    for (; j + 96 < f.nw; j += 128) { // four independent loads in flight
+      const int a0 = f.w[j] + row[j], a1 = f.w[j + 32] + row[j + 32];
+      const int a2 = f.w[j + 64] + row[j + 64], a3 = f.w[j + 96] + row[j + 96];
+      m = min(m, min(min(a0, a1), min(a2, a3)));
+    }
+    for (; j < f.nw; j += 32) m = min(m, f.w[j] + row[j]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) f.ra[i] = m;
     return;
   }
-  // columns: 32 per block, 8 j-lanes each, then a shared-memory min over lanes
+  // columns: block (column block, j segment); 8 j-lanes x kMpRedColJ / 8 rows
   __shared__ int part[8][33];
-  const int kc = static_cast<int>(rb - row_blocks) * 32 + (threadIdx.x & 31), lane_j = threadIdx.x >> 5;
+  const int64_t cbk = rb - row_blocks;
+  const int seg = static_cast<int>(cbk % f.col_segs);
+  const int kc = static_cast<int>(cbk / f.col_segs) * 32 + (threadIdx.x & 31), lane_j = threadIdx.x >> 5;
+  const int jend = min(f.nw, (seg + 1) * kMpRedColJ);
   int m = INT_MAX;
-  if (kc < f.nv)
-    for (int j = lane_j; j < f.nw; j += 8) m = min(m, f.t2[static_cast<int64_t>(j) * f.nv + kc]);
+  if (kc < f.nv) {
+    int j = seg * kMpRedColJ + lane_j;
+    for (; j + 24 < jend; j += 32) { // four independent loads in flight
+      const int a0 = f.t2[static_cast<int64_t>(j) * f.nv + kc], a1 = f.t2[static_cast<int64_t>(j + 8) * f.nv + kc];
+      const int a2 = f.t2[static_cast<int64_t>(j + 16) * f.nv + kc], a3 = f.t2[static_cast<int64_t>(j + 24) * f.nv + kc];
+      m = min(m, min(min(a0, a1), min(a2, a3)));
+    }
+    for (; j < jend; j += 8) m = min(m, f.t2[static_cast<int64_t>(j) * f.nv + kc]);
+  }
   part[lane_j][threadIdx.x & 31] = m;
   __syncthreads();
   if (threadIdx.x < 32 && kc < f.nv) {
     int r = part[0][threadIdx.x];
 #pragma unroll
     for (int q = 1; q < 8; ++q) r = min(r, part[q][threadIdx.x]);
-    f.cb[kc] = r;
+    f.cbp[static_cast<int64_t>(seg) * f.nv + kc] = r;
   }
+}
+
+// cb[k] = min over the column's segment minima
+__device__ __forceinline__ int mp_colmin(const MpFold &f, int k) {
+  int m = f.cbp[k];
+  for (int s = 1; s < f.col_segs; ++s) m = min(m, f.cbp[static_cast<int64_t>(s) * f.nv + k]);
+  return m;
 }
 
 // ---- mp_pack: 32x32 tiles; A part over (i, j) then B part over (j, k) -------
@@ -139,10 +166,12 @@ __global__ void __launch_bounds__(256) mp_pack_kernel(const MpFold *folds, int n
   }
   pb -= static_cast<int64_t>(ti_a) * tj;
   const int j0 = static_cast<int>(pb / tk) * 32, k0 = static_cast<int>(pb % tk) * 32;
+  const int cbk = k0 + tx < f.nv ? mp_colmin(f, k0 + tx) : 0;
+  if (j0 == 0 && ty == 0 && k0 + tx < f.nv) f.cb[k0 + tx] = cbk; // for mp_rescan
   for (int r = ty; r < 32; r += 8) { // row j = j0 + r, col k = k0 + tx
     const int j = j0 + r, k = k0 + tx;
     int v = kMpPad;
-    if (j < f.nw && k < f.nv) v = f.t2[static_cast<int64_t>(j) * f.nv + k] - f.cb[k];
+    if (j < f.nw && k < f.nv) v = f.t2[static_cast<int64_t>(j) * f.nv + k] - cbk;
     tile[r][tx] = v;
     f.B16[static_cast<int64_t>(j) * f.nvp + k] = static_cast<uint16_t>(v);
   }

@@ -31,12 +31,14 @@ static int env_int(const char *name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 struct Knobs {
-  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, panel, panel_side, chains, chain_path, rotate,
+  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, panel, panel_side, chains,
+      chain_path, rotate,
       wave_trace, stage, blocks_per_sm;
   Knobs()
       : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
         chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
-        chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), panel(env_int("PARPLAN_PANEL", 1)),
+        chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), mp_split_penalty_milli(env_int("PARPLAN_MP_SPLIT_PENALTY", 250)),
+        panel(env_int("PARPLAN_PANEL", 1)),
         panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
         chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
         wave_trace(env_int("PARPLAN_WAVE_TRACE", 0)), stage(env_int("PARPLAN_STAGE", 1)),
@@ -245,8 +247,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // rowspan(w + t1) <= 16383 and colspan(t2) <= 16382 (minplus.cuh).
   std::vector<char> large(s.ops.size(), 0);
   struct MpLayout {
-    size_t ra, cb, A2T, A16, B16, B16T, P;
-    int nup, nwp, nvp, splits, cps;
+    size_t ra, cb, cbp, A2T, A16, B16, B16T, P;
+    int nup, nwp, nvp, splits, cps, segs;
   };
   std::vector<MpLayout> mpl(s.ops.size());
   size_t mp_bytes = 0;
@@ -279,7 +281,25 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         tiles += static_cast<int64_t>((nu_eff(op.e1) + kMpTile - 1) / kMpTile) *
                  ((cols[static_cast<size_t>(op.e2)] + kMpTile - 1) / kMpTile);
       }
-      const int64_t want = std::max<int64_t>(1, (2 * int64_t(ctx->sms) + tiles - 1) / std::max<int64_t>(1, tiles));
+      // split-j factor: minimise the makespan ceil(tiles * s / cap) / s of one
+      // launch (cap = co-resident mp_fold CTAs), with a small per-split cost
+      // for the packed-key atomics and the P initialisation
+      int64_t want = std::max<int64_t>(1, (2 * int64_t(ctx->sms) + tiles - 1) / std::max<int64_t>(1, tiles));
+      if (tiles > 0 && kn.mp_split_penalty_milli >= 0) {
+        want = 1;
+        static int mp_occ = 0;
+        if (!mp_occ) {
+          PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
+          PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mp_occ, mp_fold_kernel, kMpThreads, kMpSmem));
+          mp_occ = std::max(mp_occ, 1);
+        }
+        const double cap = static_cast<double>(ctx->sms) * mp_occ;
+        double best = 1e30;
+        for (int64_t sp = 1; sp <= 64; ++sp) {
+          const double cost = std::ceil(static_cast<double>(tiles * sp) / cap) / static_cast<double>(sp) + 0.001 * kn.mp_split_penalty_milli * sp;
+          if (cost < best - 1e-12) best = cost, want = sp;
+        }
+      }
       size_t off = 0;
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
@@ -303,6 +323,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         };
         L.ra = take(static_cast<size_t>(nu) * 4);
         L.cb = take(static_cast<size_t>(nv) * 4);
+        L.segs = (nw + kMpRedColJ - 1) / kMpRedColJ;
+        L.cbp = take(static_cast<size_t>(L.segs) * nv * 4);
         L.A2T = take(static_cast<size_t>(L.nwp) * L.nup * 4);
         L.A16 = take(static_cast<size_t>(nu) * L.nwp * 2);
         L.B16 = take(static_cast<size_t>(L.nwp) * L.nvp * 2);
@@ -461,6 +483,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
             f.ra = reinterpret_cast<int32_t *>(sb + L.ra);
             f.cb = reinterpret_cast<int32_t *>(sb + L.cb);
+            f.cbp = reinterpret_cast<int32_t *>(sb + L.cbp);
+            f.col_segs = L.segs;
             f.A2T = reinterpret_cast<uint32_t *>(sb + L.A2T);
             f.A16 = reinterpret_cast<uint16_t *>(sb + L.A16);
             f.B16 = reinterpret_cast<uint16_t *>(sb + L.B16);
@@ -477,7 +501,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             f.fold_begin = wr.fold_blocks;
             wr.fold_blocks += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.splits;
             f.red_begin = wr.red_blocks;
-            wr.red_blocks += (f.nu + kMpRedRowsPerBlock - 1) / kMpRedRowsPerBlock + (f.nv + 31) / 32;
+            wr.red_blocks += (f.nu + kMpRedRowsPerBlock - 1) / kMpRedRowsPerBlock + static_cast<int64_t>((f.nv + 31) / 32) * L.segs;
             f.pack_begin = wr.pack_blocks;
             wr.pack_blocks += static_cast<int64_t>(f.nup / 32) * (f.nwp / 32) + static_cast<int64_t>(f.nwp / 32) * (f.nvp / 32);
             f.rescan_begin = wr.rescan_blocks;
