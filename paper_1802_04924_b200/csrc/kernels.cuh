@@ -16,6 +16,8 @@
 
 namespace pp {
 
+constexpr int kMaxEpi = 4;
+
 template <class T> struct FoldDesc {
   const T *t1; // [nu][nw]
   const T *t2; // [nw][nv]
@@ -27,7 +29,24 @@ template <class T> struct FoldDesc {
   int64_t tile_begin; // first global tile id of this fold
   int32_t small;      // tile mode: 0 32x32 chunked, 1 16x16 chunked, kPanel16/8/4 panel tiles (nw <= kPanel)
   int32_t late;       // fused kernel: operands written by the previous wave (kPanelT1 | kPanelT2)
+  // fused kernel: edge eliminations absorbed into this fold (Eq. 3 merges
+  // whose other operand is ready before it runs): out = ((v + epi[0]) + epi[1]) ...,
+  // one IEEE add per merge in the reference's merge order
+  const T *epi[kMaxEpi];  // added table; with epi2: the merge (epi + epi2) is added
+  const T *epi2[kMaxEpi];
+  int32_t n_epi;
+  int32_t pad;
 };
+
+// v with the fold's absorbed merges added, cell o of the [nu][nv] output
+template <class T> __device__ __forceinline__ T fold_epilogue(const FoldDesc<T> &f, int64_t o, T v) {
+  for (int e = 0; e < f.n_epi; ++e) {
+    T x = __ldcg(&f.epi[e][o]);
+    if (f.epi2[e]) x = x + __ldcg(&f.epi2[e][o]);
+    v = v + x;
+  }
+  return v;
+}
 
 // Panel tiles: small-wave folds with nw <= kPanel stage the whole j range of
 // an R x R output tile in shared memory with one batch of loads (one memory
@@ -242,7 +261,8 @@ __device__ __forceinline__ void panel_tile_r(const FoldDesc<T> &f, int64_t tile,
   const int k = static_cast<int>(tile % f.tiles_k) * R + tx;
   if (tr && threadIdx.x == 0) tr[6] = trace_ns();
   if (g == 0 && i < f.nu && k < f.nv) {
-    f.out[static_cast<int64_t>(i) * f.nv + k] = Ar[j0] + Bc[j0 * kRS]; // the winner's own sum (keeps -0.0)
+    const int64_t o = static_cast<int64_t>(i) * f.nv + k;
+    f.out[o] = fold_epilogue(f, o, Ar[j0] + Bc[j0 * kRS]); // the winner's own sum (keeps -0.0)
     f.am[static_cast<int64_t>(i) * f.nv + k] = static_cast<uint16_t>(j0);
   }
   __syncthreads();
@@ -489,6 +509,7 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
       const int64_t o = static_cast<int64_t>(r0 + r) * nv + v;
       f.am[o] = static_cast<uint16_t>(j);
       if (c.path) amS[(k * c.rows + r) * kChainMax + v] = static_cast<uint16_t>(j);
+      b = fold_epilogue(f, o, b);
       if (last)
         f.out[o] = b;
       else
@@ -603,7 +624,7 @@ __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds,
       const int i = i0 + ty, k = k0 + tx;
       if (i < f.nu && k < f.nv) {
         const bool odd = jo >= 0 && (bo < be || (bo == be && jo < je));
-        f.out[static_cast<int64_t>(i) * f.nv + k] = odd ? bo : be;
+        f.out[static_cast<int64_t>(i) * f.nv + k] = fold_epilogue(f, static_cast<int64_t>(i) * f.nv + k, odd ? bo : be);
         f.am[static_cast<int64_t>(i) * f.nv + k] = static_cast<uint16_t>(odd ? jo : je);
       }
       return;
@@ -671,7 +692,8 @@ __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds,
         const int k = k0 + tx + c;
         if (k < f.nv) {
           const bool odd = jo[c] >= 0 && (bo[c] < be[c] || (bo[c] == be[c] && jo[c] < je[c]));
-          f.out[static_cast<int64_t>(i) * f.nv + k] = odd ? bo[c] : be[c];
+          f.out[static_cast<int64_t>(i) * f.nv + k] =
+              fold_epilogue(f, static_cast<int64_t>(i) * f.nv + k, odd ? bo[c] : be[c]);
           f.am[static_cast<int64_t>(i) * f.nv + k] = static_cast<uint16_t>(odd ? jo[c] : je[c]);
         }
       }

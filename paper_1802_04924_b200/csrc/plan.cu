@@ -31,13 +31,15 @@ static int env_int(const char *name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 struct Knobs {
-  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, panel, panel_side, chains,
+  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, merge_fuse, panel,
+      panel_side, chains,
       chain_path, rotate,
       wave_trace, stage, blocks_per_sm;
   Knobs()
       : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
         chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
         chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), mp_split_penalty_milli(env_int("PARPLAN_MP_SPLIT_PENALTY", 250)),
+        merge_fuse(env_int("PARPLAN_MERGE_FUSE", 1)),
         panel(env_int("PARPLAN_PANEL", 1)),
         panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
         chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
@@ -389,6 +391,112 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     size_t res_bytes;
   };
   const bool use_fused = mp_bytes == 0 && !ctx->no_fused && !shard;
+  // ---- effective schedule of the fused kernel: merge absorption ------------
+  // An edge elimination (Eq. 3, out = a + b) whose operand a comes from a fold
+  // F (or from merges already absorbed into F) while b is ready before F runs
+  // is folded into F's epilogue: F writes ((v + b1) + b2)..., one IEEE add per
+  // merge in the reference's order (a single add is commutative, so which
+  // operand F produced does not matter).  Merge-only waves disappear and later
+  // folds move up.  Needs every derived table kept (keep_all: no memory reuse
+  // across the reordered waves).
+  const int n_ops = static_cast<int>(s.ops.size());
+  std::vector<int> out_table(static_cast<size_t>(n_ops)), op_wave(static_cast<size_t>(n_ops));
+  std::vector<std::vector<std::pair<int, int>>> epi(static_cast<size_t>(n_ops)); // (table, table or -1) per absorbed merge
+  std::vector<char> absorbed(static_cast<size_t>(n_ops), 0);
+  std::vector<int> tab_wave(static_cast<size_t>(E_total), 0); // effective wave writing each table
+  int EWn = s.n_waves;
+  std::vector<int> EWbegin(s.wave_begin.begin(), s.wave_begin.end()), EWexec(s.exec.begin(), s.exec.end());
+  for (int oi = 0; oi < n_ops; ++oi) out_table[static_cast<size_t>(oi)] = s.ops[static_cast<size_t>(oi)].ne;
+  for (int oi = 0; oi < n_ops; ++oi) op_wave[static_cast<size_t>(oi)] = s.ops[static_cast<size_t>(oi)].wave;
+  for (int id = 0; id < E_total; ++id) tab_wave[static_cast<size_t>(id)] = prod_wave[static_cast<size_t>(id)];
+  if (use_fused && keep_all && kn.merge_fuse) {
+    // runs of fold-only waves that may become chain segments (original waves,
+    // ignoring shared-memory limits): a host fold inside one only absorbs
+    // operands written before the run, so absorption never breaks a segment
+    std::vector<int> run_start(static_cast<size_t>(s.n_waves) + 2, 0);
+    for (int w = 1; w <= s.n_waves; ++w) {
+      bool folds_only = true;
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x)
+        folds_only = folds_only && !s.ops[static_cast<size_t>(s.exec[static_cast<size_t>(x)])].type;
+      int ws = w;
+      if (folds_only && w > 1 && run_start[static_cast<size_t>(w) - 1] > 0) {
+        const int cand = run_start[static_cast<size_t>(w) - 1];
+        bool ok = true;
+        for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x)
+          ok = ok && prod_wave[static_cast<size_t>(s.ops[static_cast<size_t>(s.exec[static_cast<size_t>(x)])].e2)] < cand;
+        if (ok) ws = cand;
+      }
+      run_start[static_cast<size_t>(w)] = folds_only ? ws : 0;
+    }
+    std::vector<int> owner(static_cast<size_t>(E_total), -1);    // fold writing a table (after absorption)
+    std::vector<int> merge_of(static_cast<size_t>(E_total), -1); // real merge writing a table
+    for (int id = 0; id < E_total; ++id) tab_wave[static_cast<size_t>(id)] = 0;
+    for (int w = 1; w <= s.n_waves; ++w)
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        const int wa = tab_wave[static_cast<size_t>(op.e1)], wb = tab_wave[static_cast<size_t>(op.e2)];
+        if (!op.type) {
+          const int ew = 1 + std::max(wa, wb);
+          op_wave[static_cast<size_t>(oi)] = ew;
+          tab_wave[static_cast<size_t>(op.ne)] = ew;
+          owner[static_cast<size_t>(op.ne)] = oi;
+          continue;
+        }
+        // operands must be ready before the host runs (before its fold run,
+        // when it sits in one); a not-yet-absorbed merge of two such tables
+        // rides along as a pair
+        int host = -1;
+        std::pair<int, int> add{-1, -1};
+        for (int side = 0; side < 2 && host < 0; ++side) {
+          const int mine = side ? op.e2 : op.e1, oth = side ? op.e1 : op.e2;
+          const int F = owner[static_cast<size_t>(mine)];
+          if (F < 0 || out_table[static_cast<size_t>(F)] != mine || epi[static_cast<size_t>(F)].size() >= kMaxEpi) continue;
+          const int rs = run_start[static_cast<size_t>(s.ops[static_cast<size_t>(F)].wave)];
+          const int lim = rs > 0 ? std::min(op_wave[static_cast<size_t>(F)], rs) : op_wave[static_cast<size_t>(F)];
+          auto old_enough = [&](int id) { return tab_wave[static_cast<size_t>(id)] == 0 || tab_wave[static_cast<size_t>(id)] < lim; };
+          if (old_enough(oth)) {
+            host = F, add = {oth, -1};
+          } else if (merge_of[static_cast<size_t>(oth)] >= 0) {
+            const int M2 = merge_of[static_cast<size_t>(oth)];
+            const Op &o2 = s.ops[static_cast<size_t>(M2)];
+            if (!absorbed[static_cast<size_t>(M2)] && old_enough(o2.e1) && old_enough(o2.e2)) {
+              host = F, add = {o2.e1, o2.e2};
+              absorbed[static_cast<size_t>(M2)] = 1;
+            }
+          }
+        }
+        if (host >= 0) {
+          epi[static_cast<size_t>(host)].push_back(add);
+          out_table[static_cast<size_t>(host)] = op.ne;
+          owner[static_cast<size_t>(op.ne)] = host;
+          tab_wave[static_cast<size_t>(op.ne)] = op_wave[static_cast<size_t>(host)];
+          absorbed[static_cast<size_t>(oi)] = 1;
+        } else {
+          const int ew = 1 + std::max(wa, wb);
+          op_wave[static_cast<size_t>(oi)] = ew;
+          tab_wave[static_cast<size_t>(op.ne)] = ew;
+          merge_of[static_cast<size_t>(op.ne)] = oi;
+        }
+      }
+    // regroup the surviving ops by effective wave (stable: schedule order within a wave)
+    EWn = 0;
+    for (int oi = 0; oi < n_ops; ++oi)
+      if (!absorbed[static_cast<size_t>(oi)]) EWn = std::max(EWn, op_wave[static_cast<size_t>(oi)]);
+    std::vector<std::vector<int>> by(static_cast<size_t>(EWn) + 1);
+    for (int w = 1; w <= s.n_waves; ++w)
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        if (!absorbed[static_cast<size_t>(oi)]) by[static_cast<size_t>(op_wave[static_cast<size_t>(oi)])].push_back(oi);
+      }
+    EWbegin.assign(static_cast<size_t>(EWn) + 2, 0);
+    EWexec.clear();
+    for (int w = 1; w <= EWn; ++w) {
+      EWbegin[static_cast<size_t>(w)] = static_cast<int>(EWexec.size());
+      EWexec.insert(EWexec.end(), by[static_cast<size_t>(w)].begin(), by[static_cast<size_t>(w)].end());
+    }
+    EWbegin[static_cast<size_t>(EWn) + 1] = static_cast<int>(EWexec.size());
+  }
   // fused kernel: waves with at most kNarrowItems work items run on the first
   // thread-block cluster alone, with cluster barriers between consecutive
   // narrow waves instead of grid-wide ones
@@ -431,13 +539,13 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<FoldOps> fold_ops;
     std::vector<MergeDesc<T>> merges;
     std::vector<MpFold> mpf;
-    for (int w = 1; w <= s.n_waves; ++w) {
+    for (int w = 1; w <= EWn; ++w) {
       WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, 0, 0, 0.0, {}, {}};
       // a wave whose generic folds cover fewer than 2 x SMs 32x32 tiles uses
       // 16x16 tiles: 4x the blocks, a quarter of the per-tile latency
       int64_t big_tiles = 0;
-      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = s.exec[static_cast<size_t>(x)];
+      for (int x = EWbegin[static_cast<size_t>(w)]; x < EWbegin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = EWexec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
         if (op.type || large[static_cast<size_t>(oi)]) continue;
         big_tiles += static_cast<int64_t>((nu_eff(op.e1) + kTile - 1) / kTile) *
@@ -452,9 +560,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         for (int mode : {kPanel4, kPanel8}) {
           const int R = panel_side(mode);
           int64_t n = 0;
-          for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-            const Op &op = s.ops[static_cast<size_t>(s.exec[static_cast<size_t>(x)])];
-            if (op.type || large[static_cast<size_t>(s.exec[static_cast<size_t>(x)])]) continue;
+          for (int x = EWbegin[static_cast<size_t>(w)]; x < EWbegin[static_cast<size_t>(w) + 1]; ++x) {
+            const Op &op = s.ops[static_cast<size_t>(EWexec[static_cast<size_t>(x)])];
+            if (op.type || large[static_cast<size_t>(EWexec[static_cast<size_t>(x)])]) continue;
             n += static_cast<int64_t>((nu_eff(op.e1) + R - 1) / R) * ((cols[static_cast<size_t>(op.e2)] + R - 1) / R);
           }
           if (forced ? R == forced : n <= 2 * int64_t(ctx->sms)) {
@@ -463,10 +571,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           }
         }
       }
-      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = s.exec[static_cast<size_t>(x)];
+      for (int x = EWbegin[static_cast<size_t>(w)]; x < EWbegin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = EWexec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
-        T *out = const_cast<T *>(tabp(op.ne));
+        T *out = const_cast<T *>(tabp(out_table[static_cast<size_t>(oi)]));
         if (shard && !op.type && op.e2 >= t.ne)
           wr.gathers.emplace_back(tabp(op.e2), gatp(op.e2),
                                   static_cast<size_t>(blk(op.e2)) * cols[static_cast<size_t>(op.e2)] * sizeof(T));
@@ -514,7 +622,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           }
         }
         if (!op.type) {
-          FoldDesc<T> f;
+          FoldDesc<T> f{};
           f.t1 = rowp(op.e1);
           f.t2 = t2p(op.e2);
           f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
@@ -526,7 +634,13 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           f.small = small_wave ? (f.nw <= kPanel && kn.panel ? panel_mode : 1) : 0;
           const int ts = f.small >= kPanel16 ? panel_side(f.small) : f.small ? kSmallTile : kTile;
           f.late = 0; // set below, once the narrow waves are known
-          fold_ops.push_back({op.e1, op.e2, op.ne, w, oi});
+          fold_ops.push_back({op.e1, op.e2, out_table[static_cast<size_t>(oi)], w, oi});
+          f.n_epi = static_cast<int32_t>(epi[static_cast<size_t>(oi)].size());
+          for (int e = 0; e < f.n_epi; ++e) {
+            const auto &ab = epi[static_cast<size_t>(oi)][static_cast<size_t>(e)];
+            f.epi[e] = tabp(ab.first);
+            f.epi2[e] = ab.second >= 0 ? tabp(ab.second) : nullptr;
+          }
           f.tiles_k = (f.nv + ts - 1) / ts;
           f.tile_begin = wr.ftiles;
           wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
@@ -552,7 +666,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     // operands of a wave's first item may be staged during the previous wave:
     // those every block has seen through a grid barrier that ended a wave
     // x <= w - 2 (a narrow-to-narrow step ends in a cluster barrier only)
-    const int nwv = s.n_waves;
+    const int nwv = EWn;
     // chain segments (fused kernel, chain_item): maximal runs of >= 2 waves of
     // folds only, each fold's t2 written before the run and its t1 before the
     // run or by a fold of the run (whose chain it extends)
@@ -583,8 +697,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           const FoldOps &o = fold_ops[q];
           if (folds[q].nw > kChainMax || folds[q].nv > kChainMax) return false;
           if (chain_smem_bytes<T>(1, 64, chain_stage_bytes<T>(folds[q].nw, folds[q].nv), false) > limit) return false;
-          if (prod_wave[static_cast<size_t>(o.e2)] >= ws) return false;
-          const int p1 = prod_wave[static_cast<size_t>(o.e1)];
+          if (tab_wave[static_cast<size_t>(o.e2)] >= ws) return false;
+          for (const auto &ab : epi[static_cast<size_t>(o.oi)]) // absorbed-merge operands: written before the run too
+            if (tab_wave[static_cast<size_t>(ab.first)] >= ws || (ab.second >= 0 && tab_wave[static_cast<size_t>(ab.second)] >= ws))
+              return false;
+          const int p1 = tab_wave[static_cast<size_t>(o.e1)];
           if (p1 >= ws && p1 >= w) return false;
         }
         return true;
@@ -624,7 +741,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             const WaveRange &wr = im.waves[static_cast<size_t>(x) - 1];
             for (size_t q = wr.f0; q < wr.f0 + static_cast<size_t>(wr.nf); ++q) {
               const FoldOps &o = fold_ops[q];
-              int c = prod_wave[static_cast<size_t>(o.e1)] >= w ? chain_of_table[static_cast<size_t>(o.e1)] : -1;
+              int c = tab_wave[static_cast<size_t>(o.e1)] >= w ? chain_of_table[static_cast<size_t>(o.e1)] : -1;
               if (c < 0) {
                 c = static_cast<int>(members.size());
                 members.emplace_back();
@@ -687,8 +804,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     for (size_t q = 0; q < folds.size(); ++q) {
       const FoldOps &o = fold_ops[q];
       const int vis = seen[static_cast<size_t>(o.wave)];
-      folds[q].late = (prod_wave[static_cast<size_t>(o.e1)] > vis ? kPanelT1 : 0) |
-                      (prod_wave[static_cast<size_t>(o.e2)] > vis || (shard && o.e2 >= t.ne) ? kPanelT2 : 0);
+      folds[q].late = (tab_wave[static_cast<size_t>(o.e1)] > vis ? kPanelT1 : 0) |
+                      (tab_wave[static_cast<size_t>(o.e2)] > vis || (shard && o.e2 >= t.ne) ? kPanelT2 : 0);
     }
     std::vector<EnumNode> en(static_cast<size_t>(K));
     for (int d = 0; d < K; ++d) {
@@ -715,9 +832,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     // unwind records grouped by wave, last wave first (kernels.cuh finish_kernel)
     std::vector<UnwindRec> recs;
     std::vector<int32_t> groups{0};
-    for (int w = s.n_waves; w >= 1; --w) {
-      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = s.exec[static_cast<size_t>(x)];
+    for (int w = EWn; w >= 1; --w) {
+      for (int x = EWbegin[static_cast<size_t>(w)]; x < EWbegin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = EWexec[static_cast<size_t>(x)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
         if (op.type) continue;
         const int ch = chain_of_op[static_cast<size_t>(oi)];
