@@ -31,7 +31,8 @@ static int env_int(const char *name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 struct Knobs {
-  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, merge_fuse, panel,
+  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, merge_fuse,
+      chain_min_waves, early_build, panel,
       panel_side, chains,
       chain_path, rotate,
       wave_trace, stage, blocks_per_sm;
@@ -39,7 +40,8 @@ struct Knobs {
       : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
         chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
         chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), mp_split_penalty_milli(env_int("PARPLAN_MP_SPLIT_PENALTY", 250)),
-        merge_fuse(env_int("PARPLAN_MERGE_FUSE", 1)),
+        merge_fuse(env_int("PARPLAN_MERGE_FUSE", 1)), chain_min_waves(std::max(2, env_int("PARPLAN_CHAIN_MIN_WAVES", 2))),
+        early_build(env_int("PARPLAN_EARLY_BUILD", 1)),
         panel(env_int("PARPLAN_PANEL", 1)),
         panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
         chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
@@ -112,6 +114,7 @@ struct pp_prepared {
   std::vector<int32_t> step_kind; // 0 K1/K2, 1 wave, 2 K5, 3 finish, 4 D2H
   std::vector<double> step_work;  // cells: K1/K2 table cells, wave min-plus cells (nu*nw*nv) + merge cells
   bool launched = false, uploaded = false;
+  bool early_built = false; // transient plan: the table build was launched during prepare (ev0 already recorded)
   size_t stamp_off = 0; // fused kernel phase stamps (image offset), n_stamps entries
   int n_stamps = 0;
   size_t trace_off = 0; // PARPLAN_WAVE_TRACE: 8 stamps per wave (printed by pp_plan_profile)
@@ -503,6 +506,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   const int fused_nc = use_fused ? std::max(1, kn.cluster) : 1;
   const int64_t narrow_items = use_fused ? kn.narrow_items : 0;
   const size_t kChainSmemMax = static_cast<size_t>(kn.chain_smem_kb) * 1024;
+  bool early = false; // transient plans: K1/K2 launched before the image is built
   // sb: base of the device-only scratch section (buffers the kernels write:
   // enumeration block results, cost terms, stamps, chain path tables), not uploaded
   auto make_image = [&](unsigned char *db, unsigned char *sb) {
@@ -712,7 +716,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           int we = w;
           if (fits(w, w, limit))
             while (we + 1 <= nwv && fits(we + 1, w, limit)) ++we;
-          if (we > w) r.emplace_back(w, we);
+          if (we - w + 1 >= kn.chain_min_waves) r.emplace_back(w, we);
           w = we + 1;
         }
         return r;
@@ -908,7 +912,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     im.oS = pk.put(es);
     im.oD = pk.put(ed);
     im.oC = pk.put(t.counts);
-    if (bp) {
+    if (bp && !early) {
       im.oLay = pk.put(bp->L);
       im.oEdg = pk.put(bp->E);
       im.oCfg = pk.put(*bp->cfg32);
@@ -932,9 +936,62 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // pool and rebuild only when the pool has to grow (first calls).
   Image im;
   if (P->transient) {
+    // One-shot plans overlap the host's descriptor build with the device's
+    // table build: K1/K2 launch first (their descriptors go up in a small
+    // separate upload), the image is built while they run, and the fused
+    // kernel follows without its build phase.  The pool must already hold
+    // the final layout; if the image outgrows the estimate, fall back.
+    if (bp && use_fused && bp->grid > 0 && kn.early_build && ctx->last_image_bytes > 0) {
+      ctx->plan_pool.ensure(off_image + align256(ctx->last_image_bytes + ctx->last_image_bytes / 4 + 65536));
+      unsigned char *pb = ctx->plan_pool.p;
+      // descriptor arrays straight into pinned staging, one H2D copy
+      size_t o = 0;
+      auto slot = [&](size_t bytes) {
+        const size_t at = o;
+        o = (o + bytes + 15) & ~size_t(15);
+        return at;
+      };
+      const size_t oL = slot(bp->L.size() * sizeof(LayerDev)), oE = slot(bp->E.size() * sizeof(EdgeDev)),
+                   oC = slot(bp->cfg32->size() * 4), oR = slot(bp->rates.size() * 8), oB = slot(bp->bw.size() * 8);
+      unsigned char *h = static_cast<unsigned char *>(ctx->staging.ensure(o + 16));
+      std::memcpy(h + oL, bp->L.data(), bp->L.size() * sizeof(LayerDev));
+      std::memcpy(h + oE, bp->E.data(), bp->E.size() * sizeof(EdgeDev));
+      std::memcpy(h + oC, bp->cfg32->data(), bp->cfg32->size() * 4);
+      std::memcpy(h + oR, bp->rates.data(), bp->rates.size() * 8);
+      std::memcpy(h + oB, bp->bw.data(), bp->bw.size() * 8);
+      ctx->desc.ensure(o + 16);
+      ctx->begin(); // the plan's device time starts with the table build
+      unsigned char *base = ctx->desc.p;
+      PP_CUDA(cudaMemcpyAsync(base, h, o, cudaMemcpyHostToDevice, ctx->stream));
+      BuildArgs a{};
+      a.layers = reinterpret_cast<const LayerDev *>(base + oL);
+      a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
+      a.cfg = reinterpret_cast<const int32_t *>(base + oC);
+      a.rates = reinterpret_cast<const double *>(base + oR);
+      a.bw = reinterpret_cast<const double *>(base + oB);
+      const size_t nb = align256(static_cast<size_t>(t.ncells) * 8);
+      a.node = reinterpret_cast<double *>(pb + off_tables);
+      a.compute = reinterpret_cast<double *>(pb + off_tables + nb);
+      a.sync = reinterpret_cast<double *>(pb + off_tables + 2 * nb);
+      a.xfer = reinterpret_cast<double *>(pb + off_tables + 3 * nb);
+      a.ncells = t.ncells;
+      a.nl = t.nl, a.ne = t.ne, a.D = bp->D;
+      a.node_blocks = static_cast<int32_t>(bp->node_blocks);
+      a.bw_uniform = bp->bw_uniform;
+      clk.mark("early-upload");
+      launch_build(ctx, ctx->stream, a, bp->grid);
+      clk.mark("early-launch");
+      early = true;
+      P->early_built = true;
+    }
     im = make_image(ctx->plan_pool.p, ctx->plan_scratch.p);
     const size_t total = off_image + align256(im.pk.size());
     if (total > ctx->plan_pool.n || !ctx->plan_pool.p || im.scratch > ctx->plan_scratch.n || !ctx->plan_scratch.p) {
+      if (early) { // the pool moves: rebuild the tables in the fused kernel instead
+        PP_CUDA(cudaStreamSynchronize(ctx->stream));
+        early = false;
+        P->early_built = false;
+      }
       ctx->plan_pool.ensure(total + total / 4);
       ctx->plan_scratch.ensure(std::max<size_t>(im.scratch + im.scratch / 4, 256));
       im = make_image(ctx->plan_pool.p, ctx->plan_scratch.p);
@@ -996,7 +1053,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     }
   };
   BuildArgs ba{};
-  if (bp) {
+  if (bp && !early) {
     ba.layers = reinterpret_cast<const LayerDev *>(dimg + im.oLay);
     ba.edges = reinterpret_cast<const EdgeDev *>(dimg + im.oEdg);
     ba.cfg = reinterpret_cast<const int32_t *>(dimg + im.oCfg);
@@ -1130,9 +1187,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       launches += 2;
     } else {
       FusedArgs<T> fz{};
-      fz.has_build = bp != nullptr;
+      fz.has_build = bp != nullptr && !early;
       fz.build = ba;
-      fz.xcells = bp ? t.xcells : 0;
+      fz.xcells = bp && !early ? t.xcells : 0;
       fz.waves = reinterpret_cast<const FusedWave<T> *>(dimg + im.oFW);
       fz.n_waves = static_cast<int32_t>(im.n_phases);
       fz.en = en, fz.ee = ee, fz.k = K, fz.m = m;
@@ -1170,7 +1227,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_fused_kernel<T>, kFusedThreads, dyn));
       PP_REQUIRE(occ > 0, "fused plan kernel does not fit on an SM");
       int64_t items = std::max<int64_t>(nblk, 1);
-      if (bp) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
+      if (bp && !early) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
       for (const auto &wr : im.waves) items = std::max<int64_t>(items, wr.ftiles + wr.mblocks);
       const int per_sm_env = kn.blocks_per_sm;
       const int per_sm = per_sm_env > 0 ? std::min(per_sm_env, occ) : occ;
@@ -1221,7 +1278,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   }
   // results reach the host by zero-copy stores at the end of the finish phase
   // (FinishArgs::host_res), so no D2H copy node follows
-  P->launches_per_run = launches;
+  P->launches_per_run = launches + (early ? 1 : 0);
 }
 
 static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
@@ -1245,7 +1302,10 @@ static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
 
 static void launch(pp_prepared *P, bool upload) {
   pp_context *ctx = P->ctx;
-  ctx->begin();
+  if (P->early_built)
+    PP_CUDA(cudaSetDevice(ctx->device)); // ev0 was recorded before the early table build
+  else
+    ctx->begin();
   if (upload || !P->uploaded) {
     PP_CUDA(cudaMemcpyAsync(P->dbase + P->image_off, P->hbase, P->image_bytes, cudaMemcpyHostToDevice, ctx->stream));
     P->uploaded = true;
