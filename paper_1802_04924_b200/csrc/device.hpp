@@ -120,6 +120,7 @@ struct pp_context {
   pp::DBuf<unsigned char> plan_scratch; // device-only buffers of one-shot plans
   pp::PinnedBuf plan_pinned;
   size_t last_image_bytes = 0;          // reserve hint for the next descriptor image
+  size_t last_pool_bytes = 0;           // largest one-shot plan pool so far (early table builds)
 
   void begin() const; // cudaSetDevice + record ev0
   double end_ms();    // record ev1, sync, elapsed

@@ -169,6 +169,59 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->n_waves = s.n_waves;
   P->node_ops = s.node_ops;
   P->edge_ops = s.edge_ops;
+  bool early = false; // transient plans: K1/K2 launched before the descriptor image is built
+  {
+    // One-shot plans overlap the host's descriptor build with the device's
+    // table build: K1/K2 launch first (their descriptors go up in a small
+    // separate upload), the image is built while they run, and the fused
+    // kernel follows without its build phase.  The pool must already hold
+    // the final layout; if the image outgrows the estimate, fall back.
+    if (P->transient && bp && !ctx->no_fused && ctx->nranks <= 1 && bp->grid > 0 && kn.early_build && ctx->last_pool_bytes > 0) {
+      // at least the table region (a larger final layout falls back below)
+      ctx->plan_pool.ensure(std::max(ctx->last_pool_bytes, align256(static_cast<size_t>(t.ncells) * 8) * 3 +
+                                                               align256(static_cast<size_t>(t.xcells) * 8)));
+      unsigned char *pb = ctx->plan_pool.p;
+      // descriptor arrays straight into pinned staging, one H2D copy
+      size_t o = 0;
+      auto slot = [&](size_t bytes) {
+        const size_t at = o;
+        o = (o + bytes + 15) & ~size_t(15);
+        return at;
+      };
+      const size_t oL = slot(bp->L.size() * sizeof(LayerDev)), oE = slot(bp->E.size() * sizeof(EdgeDev)),
+                   oC = slot(bp->cfg32->size() * 4), oR = slot(bp->rates.size() * 8), oB = slot(bp->bw.size() * 8);
+      unsigned char *h = static_cast<unsigned char *>(ctx->staging.ensure(o + 16));
+      std::memcpy(h + oL, bp->L.data(), bp->L.size() * sizeof(LayerDev));
+      std::memcpy(h + oE, bp->E.data(), bp->E.size() * sizeof(EdgeDev));
+      std::memcpy(h + oC, bp->cfg32->data(), bp->cfg32->size() * 4);
+      std::memcpy(h + oR, bp->rates.data(), bp->rates.size() * 8);
+      std::memcpy(h + oB, bp->bw.data(), bp->bw.size() * 8);
+      ctx->desc.ensure(o + 16);
+      ctx->begin(); // the plan's device time starts with the table build
+      unsigned char *base = ctx->desc.p;
+      PP_CUDA(cudaMemcpyAsync(base, h, o, cudaMemcpyHostToDevice, ctx->stream));
+      BuildArgs a{};
+      a.layers = reinterpret_cast<const LayerDev *>(base + oL);
+      a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
+      a.cfg = reinterpret_cast<const int32_t *>(base + oC);
+      a.rates = reinterpret_cast<const double *>(base + oR);
+      a.bw = reinterpret_cast<const double *>(base + oB);
+      const size_t nb = align256(static_cast<size_t>(t.ncells) * 8); // the table region opens the pool
+      a.node = reinterpret_cast<double *>(pb);
+      a.compute = reinterpret_cast<double *>(pb + nb);
+      a.sync = reinterpret_cast<double *>(pb + 2 * nb);
+      a.xfer = reinterpret_cast<double *>(pb + 3 * nb);
+      a.ncells = t.ncells;
+      a.nl = t.nl, a.ne = t.ne, a.D = bp->D;
+      a.node_blocks = static_cast<int32_t>(bp->node_blocks);
+      a.bw_uniform = bp->bw_uniform;
+      clk.mark("early-upload");
+      launch_build(ctx, ctx->stream, a, bp->grid);
+      clk.mark("early-launch");
+      early = true;
+      P->early_built = true;
+    }
+  }
 
   const int E_total = static_cast<int>(s.esrc.size());
   std::vector<int32_t> rows(static_cast<size_t>(E_total)), cols(static_cast<size_t>(E_total));
@@ -506,7 +559,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   const int fused_nc = use_fused ? std::max(1, kn.cluster) : 1;
   const int64_t narrow_items = use_fused ? kn.narrow_items : 0;
   const size_t kChainSmemMax = static_cast<size_t>(kn.chain_smem_kb) * 1024;
-  bool early = false; // transient plans: K1/K2 launched before the image is built
   // sb: base of the device-only scratch section (buffers the kernels write:
   // enumeration block results, cost terms, stamps, chain path tables), not uploaded
   auto make_image = [&](unsigned char *db, unsigned char *sb) {
@@ -936,54 +988,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // pool and rebuild only when the pool has to grow (first calls).
   Image im;
   if (P->transient) {
-    // One-shot plans overlap the host's descriptor build with the device's
-    // table build: K1/K2 launch first (their descriptors go up in a small
-    // separate upload), the image is built while they run, and the fused
-    // kernel follows without its build phase.  The pool must already hold
-    // the final layout; if the image outgrows the estimate, fall back.
-    if (bp && use_fused && bp->grid > 0 && kn.early_build && ctx->last_image_bytes > 0) {
-      ctx->plan_pool.ensure(off_image + align256(ctx->last_image_bytes + ctx->last_image_bytes / 4 + 65536));
-      unsigned char *pb = ctx->plan_pool.p;
-      // descriptor arrays straight into pinned staging, one H2D copy
-      size_t o = 0;
-      auto slot = [&](size_t bytes) {
-        const size_t at = o;
-        o = (o + bytes + 15) & ~size_t(15);
-        return at;
-      };
-      const size_t oL = slot(bp->L.size() * sizeof(LayerDev)), oE = slot(bp->E.size() * sizeof(EdgeDev)),
-                   oC = slot(bp->cfg32->size() * 4), oR = slot(bp->rates.size() * 8), oB = slot(bp->bw.size() * 8);
-      unsigned char *h = static_cast<unsigned char *>(ctx->staging.ensure(o + 16));
-      std::memcpy(h + oL, bp->L.data(), bp->L.size() * sizeof(LayerDev));
-      std::memcpy(h + oE, bp->E.data(), bp->E.size() * sizeof(EdgeDev));
-      std::memcpy(h + oC, bp->cfg32->data(), bp->cfg32->size() * 4);
-      std::memcpy(h + oR, bp->rates.data(), bp->rates.size() * 8);
-      std::memcpy(h + oB, bp->bw.data(), bp->bw.size() * 8);
-      ctx->desc.ensure(o + 16);
-      ctx->begin(); // the plan's device time starts with the table build
-      unsigned char *base = ctx->desc.p;
-      PP_CUDA(cudaMemcpyAsync(base, h, o, cudaMemcpyHostToDevice, ctx->stream));
-      BuildArgs a{};
-      a.layers = reinterpret_cast<const LayerDev *>(base + oL);
-      a.edges = reinterpret_cast<const EdgeDev *>(base + oE);
-      a.cfg = reinterpret_cast<const int32_t *>(base + oC);
-      a.rates = reinterpret_cast<const double *>(base + oR);
-      a.bw = reinterpret_cast<const double *>(base + oB);
-      const size_t nb = align256(static_cast<size_t>(t.ncells) * 8);
-      a.node = reinterpret_cast<double *>(pb + off_tables);
-      a.compute = reinterpret_cast<double *>(pb + off_tables + nb);
-      a.sync = reinterpret_cast<double *>(pb + off_tables + 2 * nb);
-      a.xfer = reinterpret_cast<double *>(pb + off_tables + 3 * nb);
-      a.ncells = t.ncells;
-      a.nl = t.nl, a.ne = t.ne, a.D = bp->D;
-      a.node_blocks = static_cast<int32_t>(bp->node_blocks);
-      a.bw_uniform = bp->bw_uniform;
-      clk.mark("early-upload");
-      launch_build(ctx, ctx->stream, a, bp->grid);
-      clk.mark("early-launch");
-      early = true;
-      P->early_built = true;
-    }
     im = make_image(ctx->plan_pool.p, ctx->plan_scratch.p);
     const size_t total = off_image + align256(im.pk.size());
     if (total > ctx->plan_pool.n || !ctx->plan_pool.p || im.scratch > ctx->plan_scratch.n || !ctx->plan_scratch.p) {
@@ -996,6 +1000,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       ctx->plan_scratch.ensure(std::max<size_t>(im.scratch + im.scratch / 4, 256));
       im = make_image(ctx->plan_pool.p, ctx->plan_scratch.p);
     }
+    ctx->last_pool_bytes = std::max(ctx->last_pool_bytes, off_image + align256(im.pk.size()) + 65536);
     P->dbase = ctx->plan_pool.p;
     P->sbase = ctx->plan_scratch.p;
     P->hbase = static_cast<unsigned char *>(ctx->plan_pinned.ensure(align256(im.pk.size())));
