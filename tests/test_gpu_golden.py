@@ -57,3 +57,22 @@ def test_synthetic_golden(gpu, case):
     assert [int(x) for x in r.indices] == case["indices"]
     assert float(r.cost).hex() == case["cost"]
     assert [r.final_graph_nodes, r.node_eliminations, r.edge_eliminations] == case["stats"]
+
+
+def test_one_shot_plans_in_any_order(gpu):
+    """One-shot plans reuse a grow-only pool and launch the table build before
+    the descriptor image is built; growing, shrinking and alternating graph
+    sizes must keep every result bit-identical to the reference goldens."""
+    import paper_1802_04924_b200 as P
+
+    cases = list(GOLD["builtins"])
+    order = cases + cases[::-1] + cases[::2] + cases[1::2]
+    graphs = {}
+    for case in order:
+        key = (case["model"], case["batch"], case["devices"])
+        if key not in graphs:
+            graphs[key] = (P.builtin_model(case["model"], case["batch"]), P.DeviceGraph.uniform(case["devices"]))
+        g, dev = graphs[key]
+        r = P.plan(g, dev, ctx=gpu.ctx)
+        assert [int(x) for x in r.indices] == case["indices"], key
+        assert float(r.cost).hex() == case["cost"], key
