@@ -1,8 +1,8 @@
 /* parplan/parplan.hpp — umbrella header (reference: proj/include/parplan/parplan.hpp:17-26).
  *
- * The reference umbrella also pulls in io.hpp (nlohmann-json file formats);
- * that component is out of scope for this build.  Link with
- * -lparplan_cuda (paper_1802_04924_b200/libparplan_cuda.so).
+ * io.hpp / report.hpp need nlohmann/json.hpp on the include path (see
+ * paper_1802_04924_b200/cli/Makefile).  Link with -lparplan_cuda
+ * (paper_1802_04924_b200/libparplan_cuda.so).
  */
 #pragma once
 
@@ -10,6 +10,7 @@
 #include "parplan/baselines.hpp"
 #include "parplan/cost.hpp"
 #include "parplan/graph.hpp"
+#include "parplan/io.hpp"
 #include "parplan/models.hpp"
 #include "parplan/oracle.hpp"
 #include "parplan/partition.hpp"

@@ -29,8 +29,12 @@ def test_reference_host_suites(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["ref_test_cost_model", "ref_test_planner", "ref_test_oracle"])
+@pytest.mark.parametrize("name", ["ref_test_cost_model", "ref_test_planner", "ref_test_oracle", "ref_test_io",
+                                  "ref_test_cli"])
 def test_reference_device_suites(name):
+    """test_io: network / device / strategy / measured-cost JSON and reports
+    (include/parplan/io.hpp, report.hpp); test_cli: the drop-in CLI binary
+    paper_1802_04924_b200/bin/parplan — every subcommand, exit codes 0/2/3."""
     out = run(name)
     assert ", 0 failed" in out
 
