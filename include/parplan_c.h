@@ -241,6 +241,14 @@ pp_status pp_plan_profile(pp_prepared *p, int32_t cap, double *step_ms, int32_t 
 /* evaluate_strategy by index (cost.hpp:235-255), computed on the device from the
  * device-resident tables in the pinned summation order. */
 pp_status pp_tables_total_cost(pp_tables *t, const int32_t *indices, double *cost);
+
+/* Batched evaluate_strategy / evaluate_components totals (cost.hpp:235-293) for
+ * n strategies given as config indices indices[n][n_layers]: cost[s] summed in
+ * the reference's order (nodes by layer, then edges by id), optionally the node
+ * and transfer totals (each summed from 0.0 in the same order).  One device
+ * thread per strategy; the `compare` sweeps of SURVEY §8f. */
+pp_status pp_tables_evaluate_batch(pp_tables *t, int64_t n, const int32_t *indices, double *cost, double *node_total,
+                                   double *xfer_total);
 /* brute_force_plan (oracle.hpp:52-93) on the device; LimitError text matches. */
 pp_status pp_brute_force(pp_context *ctx, const pp_graph *g, pp_tables *t, uint64_t budget, int32_t *indices,
                          double *cost, uint64_t *visited);

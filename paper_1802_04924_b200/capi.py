@@ -109,6 +109,7 @@ _SIGS = {
     "pp_tables_download": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pp_tables_build_ms": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "pp_tables_total_cost": (C.c_int, [_vp, _i32p, C.POINTER(C.c_double)]),
+    "pp_tables_evaluate_batch": (C.c_int, [_vp, C.c_int64, _i32p, _f64p, _f64p, _f64p]),
     "pp_plan": (C.c_int, [_vp, _vp, C.POINTER(_DeviceDesc), C.c_int32, _i32p, C.POINTER(_PlanResult)]),
     "pp_plan_with_tables": (C.c_int, [_vp, _vp, _vp, C.c_int32, _i32p, C.POINTER(_PlanResult)]),
     "pp_brute_force": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _i32p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
@@ -445,6 +446,17 @@ class CostTables:
         c = C.c_double()
         _check(lib().pp_tables_total_cost(self.h, np.ascontiguousarray(indices, np.int32), C.byref(c)))
         return c.value
+
+    def evaluate_batch(self, indices):
+        """(cost, node_total, transfer_total) of many strategies, indices [n, n_layers]
+        (batched evaluate_strategy / evaluate_components totals on the device)."""
+        ix = np.ascontiguousarray(indices, np.int32)
+        if ix.ndim != 2 or ix.shape[1] != len(self.counts):
+            raise InputError("evaluate_batch: indices must be [n, n_layers]")
+        n = ix.shape[0]
+        cost, node, xfer = np.zeros(n), np.zeros(n), np.zeros(n)
+        _check(lib().pp_tables_evaluate_batch(self.h, n, ix, cost, node, xfer))
+        return cost, node, xfer
 
 
 def build_cost_tables(graph: ComputationGraph, devices: DeviceGraph, ctx: Optional[Context] = None) -> CostTables:

@@ -13,6 +13,8 @@
 // Compiled with --fmad=false: every FP64 expression keeps the reference's
 // operation order and rounding.
 #include "tables.hpp"
+
+#include <type_traits>
 #include "build.cuh"
 
 #include "parplan/geometry.hpp"
@@ -211,6 +213,36 @@ __global__ void total_cost_kernel(const T *node, const T *xfer, const int64_t *c
     t += ldexp(static_cast<double>(xfer[xoff[e] + static_cast<int64_t>(idx[esrc[e]]) * counts[edst[e]] + idx[edst[e]]]),
                -shift);
   *out = t;
+}
+
+// Batched evaluation (evaluate_strategy / evaluate_components totals,
+// cost.hpp:235-293) of n strategies given as config indices [n][nl]: one
+// thread per strategy, each total summed from 0.0 in the reference's order
+// (nodes by layer, then edges by id; node and transfer totals separately).
+template <class T>
+__global__ void evaluate_batch_kernel(const T *node, const T *xfer, const int64_t *cat_off, const int64_t *xoff,
+                                      const int32_t *esrc, const int32_t *edst, const int32_t *counts,
+                                      const int32_t *idx, int64_t n, int nl, int ne, int shift, double *cost,
+                                      double *node_total, double *xfer_total) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t *ix = idx + s * nl;
+    double t = 0.0, tn = 0.0, tx = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      const double v = ldexp(static_cast<double>(node[cat_off[l] + ix[l]]), -shift);
+      t += v;
+      tn += v;
+    }
+    for (int e = 0; e < ne; ++e) {
+      const double v =
+          ldexp(static_cast<double>(xfer[xoff[e] + static_cast<int64_t>(ix[esrc[e]]) * counts[edst[e]] + ix[edst[e]]]), -shift);
+      t += v;
+      tx += v;
+    }
+    cost[s] = t;
+    if (node_total) node_total[s] = tn;
+    if (xfer_total) xfer_total[s] = tx;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -606,6 +638,47 @@ pp_status pp_tables_total_cost(pp_tables *tp, const int32_t *indices, double *co
           reinterpret_cast<int32_t *>(P(oi)), t.nl, t.ne, t.shift, reinterpret_cast<double *>(P(oo)));
     check_launch(ctx);
     PP_CUDA(cudaMemcpyAsync(cost, P(oo), 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->end_ms();
+  });
+}
+
+pp_status pp_tables_evaluate_batch(pp_tables *tp, int64_t n, const int32_t *indices, double *cost, double *node_total,
+                                   double *xfer_total) {
+  return guard([&] {
+    PP_REQUIRE(tp && (n == 0 || (indices && cost)) && n >= 0, "pp_tables_evaluate_batch: bad argument");
+    Tables &t = tp->impl;
+    pp_context *ctx = t.ctx;
+    for (int64_t s = 0; s < n; ++s)
+      for (int l = 0; l < t.nl; ++l) {
+        const int32_t x = indices[s * t.nl + l];
+        PP_REQUIRE(x >= 0 && x < t.counts[static_cast<size_t>(l)], "config index out of range");
+      }
+    if (n == 0) return;
+    Packer pk;
+    std::vector<int32_t> es(t.esrc.begin(), t.esrc.end()), ed(t.edst.begin(), t.edst.end());
+    const size_t oc = pk.put(t.cat_off), ox = pk.put(t.xoff), os = pk.put(es), od = pk.put(ed), on = pk.put(t.counts),
+                 oi = pk.put(indices, static_cast<size_t>(n) * static_cast<size_t>(t.nl));
+    DBuf<double> out(static_cast<size_t>(n) * 3);
+    ctx->begin();
+    unsigned char *b = ctx->upload(pk);
+    auto P = [&](size_t o) { return b + o; };
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(ctx->sms) * 8));
+    double *o0 = out.p, *o1 = node_total ? out.p + n : nullptr, *o2 = xfer_total ? out.p + 2 * n : nullptr;
+    auto run = [&](auto *node, auto *xf, int shift) {
+      using T = std::remove_const_t<std::remove_pointer_t<decltype(node)>>;
+      evaluate_batch_kernel<T><<<grid, 256, 0, ctx->stream>>>(
+          node, xf, reinterpret_cast<int64_t *>(P(oc)), reinterpret_cast<int64_t *>(P(ox)),
+          reinterpret_cast<int32_t *>(P(os)), reinterpret_cast<int32_t *>(P(od)), reinterpret_cast<int32_t *>(P(on)),
+          reinterpret_cast<int32_t *>(P(oi)), n, t.nl, t.ne, shift, o0, o1, o2);
+    };
+    if (t.mode == kFP64)
+      run(static_cast<const double *>(t.node.p), static_cast<const double *>(t.xfer64.p), 0);
+    else
+      run(static_cast<const int32_t *>(t.node32.p), static_cast<const int32_t *>(t.xfer32.p), t.shift);
+    check_launch(ctx);
+    PP_CUDA(cudaMemcpyAsync(cost, o0, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (node_total) PP_CUDA(cudaMemcpyAsync(node_total, o1, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (xfer_total) PP_CUDA(cudaMemcpyAsync(xfer_total, o2, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->end_ms();
   });
 }

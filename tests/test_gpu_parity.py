@@ -183,3 +183,45 @@ def test_fused_random_graphs(gpu):
         t2 = P.upload_cost_tables(g, cat, node, xfer, split)
         a, b = P.plan_with_tables(g, t), P.plan_with_tables(g, t2)
         assert list(a.indices) == list(b.indices) and a.cost == b.cost
+
+
+def _seq_sum(vals):
+    t = 0.0
+    for v in vals:
+        t += float(v)
+    return t
+
+
+@pytest.mark.parametrize("source", ["lenet5@4", "alexnet@4", "inception_chain(2)@4", "random", "synthetic"])
+def test_evaluate_batch_matches_oracle(gpu, source):
+    """Batched evaluate_strategy: every total bit-equal to the
+    oracle's in-order sums (nodes by layer, then edges by id)."""
+    import paper_1802_04924_b200 as P
+
+    rng = np.random.default_rng(7)
+    if source == "random":
+        g, t = P.random_series_parallel_graph(11, 8, 4, 0.3, 4, ctx=gpu.ctx)
+        ref = O.Instance.random(11, 8, 4, 0.3, 4, "port")
+    elif source == "synthetic":
+        g = P.series_parallel_graph(3, 40, 0.3)
+        ref = O.Instance.synthetic(3, 40, 24, 0.3, "port")
+        t = P.upload_cost_tables(g, ref.catalogs(), ref.nodes(), ref.xfers(), ctx=gpu.ctx)
+    else:
+        model, D = source.split("@")
+        g = P.builtin_model(model, 32)
+        t = P.build_cost_tables(g, P.DeviceGraph.uniform(int(D)), gpu.ctx)
+        ref = O.Instance.builtin(model, 32, "port").build_tables(int(D))
+    counts = [len(x) for x in ref.nodes()]
+    ix = np.stack([rng.integers(0, c, size=300) for c in counts], axis=1).astype(np.int32)
+    cost, node, xfer = t.evaluate_batch(ix)
+    nodes, xfers = ref.nodes(), ref.xfers()
+    src, dst, _ = g.edges()
+    for s in range(0, 300, 7):
+        row = ix[s]
+        assert cost[s] == ref.total_cost(row)
+        assert node[s] == _seq_sum(nodes[l][row[l]] for l in range(len(counts)))
+        assert xfer[s] == _seq_sum(xfers[e][row[src[e]]][row[dst[e]]] for e in range(len(src)))
+    with pytest.raises(P.InputError):
+        bad = ix.copy()
+        bad[0, 0] = counts[0]
+        t.evaluate_batch(bad)
