@@ -13,12 +13,14 @@ namespace geo = parplan::geo;
 
 constexpr int kBuildThreads = 128;
 
-__device__ __forceinline__ void node_cost_cell(const BuildArgs &a, int64_t gi) {
+// cat_off_s: the layers' catalog offsets staged in shared memory by the
+// caller (or nullptr: read from the descriptors)
+__device__ __forceinline__ void node_cost_cell(const BuildArgs &a, int64_t gi, const int64_t *cat_off_s = nullptr) {
   // layer with cat_off <= gi < cat_off + count (binary search)
   int lo = 0, hi = a.nl - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (a.layers[mid].cat_off <= gi)
+    if ((cat_off_s ? cat_off_s[mid] : a.layers[mid].cat_off) <= gi)
       lo = mid;
     else
       hi = mid - 1;

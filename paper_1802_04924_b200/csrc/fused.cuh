@@ -105,11 +105,20 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
   if (a.has_build) {
     const BuildArgs &B = a.build;
     const int64_t n = B.ncells + a.xcells;
+    // the binary searches over layers and edges read their offsets from
+    // shared memory (a dependent chain of descriptor loads otherwise)
+    int64_t *cat_off_s = reinterpret_cast<int64_t *>(fused_smem), *out_off_s = cat_off_s + B.nl;
+    const bool offs_in_smem = static_cast<size_t>(B.nl + B.ne) * 8 <= sizeof(WaveSmem<T>);
+    if (offs_in_smem) {
+      for (int l = threadIdx.x; l < B.nl; l += kFusedThreads) cat_off_s[l] = B.layers[l].cat_off;
+      for (int e = threadIdx.x; e < B.ne; e += kFusedThreads) out_off_s[e] = B.edges[e].out_off;
+      __syncthreads();
+    }
     // block-uniform trip count: xfer_cells_warp needs whole warps
     for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * kFusedThreads; g0 < n; g0 += stride) {
       const int64_t g = g0 + threadIdx.x;
       if (g < B.ncells) {
-        node_cost_cell(B, g);
+        node_cost_cell(B, g, offs_in_smem ? cat_off_s : nullptr);
       }
       int edge = -1;
       int64_t x = g - B.ncells;
@@ -117,7 +126,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
         int lo = 0, hi = B.ne - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (B.edges[mid].out_off <= x)
+          if ((offs_in_smem ? out_off_s[mid] : B.edges[mid].out_off) <= x)
             lo = mid;
           else
             hi = mid - 1;

@@ -1498,6 +1498,14 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
               std::sort(be.begin(), be.end());
               std::sort(bs.begin(), bs.end());
               std::sort(bx.begin(), bx.end());
+              if (std::getenv("PARPLAN_TRACE_BLOCKS")) {
+                std::fprintf(stderr, "build arrive by block:");
+                for (int b = 0; b < 2048; ++b) {
+                  const uint64_t x = tr[static_cast<size_t>(16 * waves + 16 + b)];
+                  if (x) std::fprintf(stderr, " %d:%.0f", b, static_cast<double>(static_cast<int64_t>(x - st[0])));
+                }
+                std::fprintf(stderr, "\n");
+              }
               std::fprintf(stderr,
                            "build: %zu blocks start min %.0f max %.0f; arrive min %.0f median %.0f p90 %.0f max %.0f; "
                            "leave min %.0f max %.0f ns (phase %.0f)\n",
