@@ -176,6 +176,27 @@ __device__ __forceinline__ int64_t xfer_maxvol_separable(const XferCell &c) {
   for (int d = 3; d >= 0; --d) {
     int bmax = -1, dfirst = 0, smax = 0, bnext = -1;
     bool nonunique = false, dvar = false;
+    // Closed forms of the x loop below.  The need interval of an
+    // x-invariant dimension (conv input channels, FC features) is the same
+    // for every x: one dim_stats, all x tie, and delta(x) - delta(0) = -x*D.
+    // An identity dimension (need = owned) whose piece sizes divide one
+    // another has the same best overlap for every x: with cd = r*cs every
+    // destination piece lies in source piece x/r (unique, second 0); with
+    // cs = r*cd (r >= 2) each covers r whole source pieces (two maximisers).
+    const bool invariant = (c.kind == geo::kConv && d == 1) || (c.kind == geo::kFC && d > 0);
+    const bool identity = c.kind == geo::kConcat ? d != c.par[0]
+                                                 : d == 0 || c.kind == geo::kSoftmax || (c.kind == geo::kPool && d == 1);
+    const bool same_extent = c.spiece[d] * c.cs[d] == c.dpiece[d] * c.cd[d];
+    if (invariant) {
+      int lo, hi;
+      need_interval(c, d, 0, c.dpiece[d], &lo, &hi);
+      const geo::DimStats<int> st = dim_stats_fast(lo, hi, c.spiece[d], c.rcp[d]);
+      bmax = st.best, nonunique = !st.unique, dvar = c.cd[d] > 1, dfirst = st.arg * S, smax = st.second;
+    } else if (identity && same_extent && c.cd[d] % c.cs[d] == 0) {
+      bmax = c.dpiece[d], dvar = c.cd[d] > 1 && (c.cd[d] != c.cs[d] || S != D);
+    } else if (identity && same_extent && c.cs[d] % c.cd[d] == 0) {
+      bmax = smax = c.spiece[d], nonunique = true, dvar = c.cd[d] > 1;
+    } else
     for (int x = 0; x < c.cd[d]; ++x) {
       const int olo = x * c.dpiece[d];
       int lo, hi;

@@ -121,6 +121,7 @@ struct pp_context {
   pp::PinnedBuf plan_pinned;
   size_t last_image_bytes = 0;          // reserve hint for the next descriptor image
   size_t last_pool_bytes = 0;           // largest one-shot plan pool so far (early table builds)
+  pp::DBuf<unsigned int> gbar;          // fused kernel: grid-barrier word [0], build chunk counter [32..33] (zeroed once)
 
   void begin() const; // cudaSetDevice + record ev0
   double end_ms();    // record ev1, sync, elapsed

@@ -57,6 +57,8 @@ template <class T> struct FusedArgs {
   int32_t stage;    // stage each wave's first item before the preceding barrier
   uint64_t *trace;  // optional: 8 stamps per wave from the block running item 0
   int32_t nc;       // cluster size (narrow waves run on blocks [0, nc))
+  unsigned int *gbar; // hand-rolled grid barrier word (scratch), nullptr: cooperative_groups grid.sync
+  unsigned long long *build_ctr; // build chunks claimed past the static first round (0 between launches)
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -66,6 +68,33 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 constexpr int kFusedThreads = 256;
+
+// Grid barrier for the cooperative launch.  Same arrive / flip protocol as
+// cooperative_groups (one atomic per CTA; the first CTA's increment flips the
+// counter's top bit once all have arrived), but the waiting thread polls with
+// relaxed loads and backs off, and the acquire is one fence after the flip:
+// the co-resident CTA of a still-working SM does not have its L1 invalidated
+// on every poll.  `bar` must start with its low 31 bits zero (they return
+// there after every barrier).
+__device__ __forceinline__ void grid_barrier(unsigned int *bar, uint64_t *ts = nullptr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    __threadfence(); // release this CTA's writes
+    if (ts) ts[0] = global_ns();
+    const unsigned int old = atomicAdd(bar, nb);
+    if (ts) ts[2048] = global_ns();
+    unsigned int cur;
+    for (;;) {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+      if ((old ^ cur) & 0x80000000u) break;
+      __nanosleep(20);
+    }
+    if (ts) ts[4096] = global_ns();
+    __threadfence(); // acquire: later reads see every CTA's writes
+  }
+  __syncthreads();
+}
 
 // Stages this block's first item of wave W: its descriptor and, for a panel
 // tile, the operands not in f.late (all of them when `ready` == kPanelAll).
@@ -99,6 +128,12 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
   WaveSmem<T> &sm = *reinterpret_cast<WaveSmem<T> *>(fused_smem);
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kFusedThreads;
   const bool stamp = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
+  auto gsync = [&] {
+    if (a.gbar)
+      grid_barrier(a.gbar);
+    else
+      grid.sync();
+  };
   int ph = 0;
   if (stamp) a.stamps[ph++] = global_ns();
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + 2048 + blockIdx.x] = global_ns();
@@ -114,9 +149,19 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
       for (int e = threadIdx.x; e < B.ne; e += kFusedThreads) out_off_s[e] = B.edges[e].out_off;
       __syncthreads();
     }
-    // block-uniform trip count: xfer_cells_warp needs whole warps
-    for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * kFusedThreads; g0 < n; g0 += stride) {
-      const int64_t g = g0 + threadIdx.x;
+    // 32-cell chunks, one per warp at a time (xfer_cells_warp needs whole
+    // warps): the first chunk of each warp is static, later ones come from a
+    // counter, so warps that drew cheap cells take more (a static grid-stride
+    // split leaves a third round on a few blocks).  The next chunk is claimed
+    // before the current one is computed: the atomic's latency overlaps it.
+    const int64_t nchunks = (n + 31) >> 5;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kFusedThreads / 32);
+    const int lane = threadIdx.x & 31;
+    int64_t chunk = static_cast<int64_t>(blockIdx.x) * (kFusedThreads / 32) + (threadIdx.x >> 5);
+    while (chunk < nchunks) {
+      unsigned long long claim = 0;
+      if (a.build_ctr && lane == 0) claim = atomicAdd(a.build_ctr, 1ull);
+      const int64_t g = (chunk << 5) + lane;
       if (g < B.ncells) {
         node_cost_cell(B, g, offs_in_smem ? cat_off_s : nullptr);
       }
@@ -135,13 +180,19 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
         x -= B.edges[lo].out_off;
       }
       xfer_cells_warp(B, edge, x);
+      chunk = a.build_ctr ? nwarps + static_cast<int64_t>(__shfl_sync(0xffffffffu, claim, 0)) : chunk + nwarps;
     }
     if (a.trace) { // per-block end of the build loop (profiling)
       __syncthreads();
       if (threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + blockIdx.x] = global_ns();
     }
-    grid.sync();
+    if (a.gbar)
+      grid_barrier(a.gbar, a.trace && blockIdx.x < 2048 ? a.trace + 16 * a.n_waves + 16 + 6144 + blockIdx.x : nullptr);
+    else
+      grid.sync();
     if (a.trace && threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + 4096 + blockIdx.x] = global_ns();
+    // every claim of this launch precedes the barrier: rearm the counter
+    if (a.build_ctr && blockIdx.x == 0 && threadIdx.x == 0) *a.build_ctr = 0;
   }
   if (stamp) a.stamps[ph++] = global_ns();
   // this block's first item of each wave is staged one wave early: its
@@ -182,7 +233,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
       // acquire at cluster scope) orders its writes; other clusters skip ahead
       if (static_cast<int>(blockIdx.x) < a.nc) cg::this_cluster().sync();
     } else {
-      grid.sync();
+      gsync();
     }
     if (tr && threadIdx.x == 0) tr[4] = global_ns();
     if (stamp) a.stamps[ph++] = global_ns();
@@ -190,7 +241,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
   using A = typename Acc<T>::type;
   for (int64_t vb = blockIdx.x; vb < a.nblk; vb += gridDim.x)
     enum_block<T>(a.en, a.k, a.ee, a.m, a.space, a.per_thread, static_cast<A *>(a.blk_val), a.blk_idx, vb);
-  grid.sync();
+  gsync();
   if (stamp) a.stamps[ph++] = global_ns();
   if (blockIdx.x == 0) finish_block<T>(a.fin, fused_smem);
   if (stamp) a.stamps[ph++] = global_ns();

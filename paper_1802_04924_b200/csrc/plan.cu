@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "minplus.cuh"
 
+#include <array>
 #include <algorithm>
 #include <cmath>
 #include <climits>
@@ -32,7 +33,7 @@ static int env_int(const char *name, int dflt) {
 }
 struct Knobs {
   int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, merge_fuse,
-      chain_min_waves, early_build, panel,
+      chain_min_waves, early_build, grid_barrier, build_dynamic, panel,
       panel_side, chains,
       chain_path, rotate,
       wave_trace, stage, blocks_per_sm;
@@ -41,7 +42,8 @@ struct Knobs {
         chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
         chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), mp_split_penalty_milli(env_int("PARPLAN_MP_SPLIT_PENALTY", 250)),
         merge_fuse(env_int("PARPLAN_MERGE_FUSE", 1)), chain_min_waves(std::max(2, env_int("PARPLAN_CHAIN_MIN_WAVES", 2))),
-        early_build(env_int("PARPLAN_EARLY_BUILD", 1)),
+        early_build(env_int("PARPLAN_EARLY_BUILD", 1)), grid_barrier(env_int("PARPLAN_GRID_BARRIER", 1)),
+        build_dynamic(env_int("PARPLAN_BUILD_DYNAMIC", 1)),
         panel(env_int("PARPLAN_PANEL", 1)),
         panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
         chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
@@ -952,7 +954,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       im.phase_chain.clear();
       for (const auto &e : fw) im.phase_chain.push_back(e.n_chains > 0);
       im.oST = scr((fw.size() + 4) * sizeof(uint64_t));
-      im.oTR = kn.wave_trace ? scr((16 * fw.size() + 16 + 6400) * sizeof(uint64_t)) + 1 : 0; // +1: nonzero flag
+      im.oTR = kn.wave_trace ? scr((16 * fw.size() + 16 + 12288) * sizeof(uint64_t)) + 1 : 0; // +1: nonzero flag
     }
     im.oN = pk.put(en);
     im.oE = pk.put(ee);
@@ -1203,6 +1205,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       fz.fin = fa;
       fz.stamps = reinterpret_cast<uint64_t *>(P->sbase + im.oST);
       fz.stage = kn.stage;
+      if (!ctx->gbar.p) { // per context: its launches are ordered on ctx->stream
+        ctx->gbar.alloc(64);
+        PP_CUDA(cudaMemsetAsync(ctx->gbar.p, 0, ctx->gbar.bytes(), ctx->stream));
+      }
+      fz.gbar = kn.grid_barrier ? ctx->gbar.p : nullptr;
+      fz.build_ctr = kn.build_dynamic ? reinterpret_cast<unsigned long long *>(ctx->gbar.p + 32) : nullptr;
       fz.trace = im.oTR ? reinterpret_cast<uint64_t *>(P->sbase + im.oTR - 1) : nullptr;
       if (fz.trace) fz.fin.trace = fz.trace + 16 * im.n_phases;
       fz.fin.smem_ok = finish_smem_bytes(t.nl, t.ne, K) <= im.dyn_smem;
@@ -1473,7 +1481,7 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
         PP_CUDA(cudaMemcpy(st.data(), P->sbase + P->stamp_off, st.size() * 8, cudaMemcpyDeviceToHost));
         const int waves = P->n_stamps - 4;
         if (P->trace_off) {
-          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves + 16 + 6400));
+          std::vector<uint64_t> tr(static_cast<size_t>(16 * waves + 16 + 12288));
           PP_CUDA(cudaMemcpy(tr.data(), P->sbase + P->trace_off - 1, tr.size() * 8, cudaMemcpyDeviceToHost));
           for (int w = 0; w < waves; ++w) {
             const uint64_t *r = &tr[static_cast<size_t>(16 * w)];
@@ -1505,6 +1513,29 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
                   if (x) std::fprintf(stderr, " %d:%.0f", b, static_cast<double>(static_cast<int64_t>(x - st[0])));
                 }
                 std::fprintf(stderr, "\n");
+              }
+              { // hand-rolled barrier internals (PARPLAN_GRID_BARRIER=1).  "arrived" is warp 0 past the
+                // block barrier, which defers blocking: the block's last warp may still be working
+                std::vector<std::array<double, 5>> q;
+                for (int b = 0; b < 2048; ++b) {
+                  const uint64_t f = tr[static_cast<size_t>(16 * waves + 16 + 6144 + b)];
+                  const uint64_t a = tr[static_cast<size_t>(16 * waves + 16 + 8192 + b)];
+                  const uint64_t e = tr[static_cast<size_t>(16 * waves + 16 + 10240 + b)];
+                  const uint64_t x = tr[static_cast<size_t>(16 * waves + 16 + b)];
+                  if (f && a && e && x)
+                    q.push_back({static_cast<double>(static_cast<int64_t>(x - st[0])),
+                                 static_cast<double>(static_cast<int64_t>(f - st[0])),
+                                 static_cast<double>(static_cast<int64_t>(a - st[0])),
+                                 static_cast<double>(static_cast<int64_t>(e - st[0])), static_cast<double>(b)});
+                }
+                if (!q.empty()) {
+                  std::sort(q.begin(), q.end(), [](const auto &x, const auto &y) { return x[2] < y[2]; });
+                  std::fprintf(stderr, "barrier by atomic time (block: arrived/fenced/atomic returned/released):");
+                  for (size_t i = 0; i < q.size(); ++i)
+                    if (i < 4 || i + 12 >= q.size())
+                      std::fprintf(stderr, " %.0f:%.0f/%.0f/%.0f/%.0f", q[i][4], q[i][0], q[i][1], q[i][2], q[i][3]);
+                  std::fprintf(stderr, "\n");
+                }
               }
               std::fprintf(stderr,
                            "build: %zu blocks start min %.0f max %.0f; arrive min %.0f median %.0f p90 %.0f max %.0f; "

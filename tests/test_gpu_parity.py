@@ -16,7 +16,12 @@ BUILTINS = [("lenet5", 1), ("lenet5", 2), ("lenet5", 4), ("alexnet", 4), ("vgg16
             ("inception_chain(3)", 2), ("inception_chain(3)", 8), ("inception_chain", 16)]
 
 
-@pytest.mark.parametrize("model,D", BUILTINS)
+# device counts whose degree sets mix factors that do not divide one another
+# (2 vs 3): K1's identity-dimension closed forms fall back to the x loop there
+ODD_D = [("lenet5", 3), ("alexnet", 6), ("inception_chain(3)", 12), ("vgg16", 6)]
+
+
+@pytest.mark.parametrize("model,D", BUILTINS + ODD_D)
 def test_tables_bit_exact(gpu, model, D):
     g = gpu.builtin(model, 32)
     t = gpu.build_tables(g, D)
