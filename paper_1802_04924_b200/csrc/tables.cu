@@ -160,7 +160,7 @@ pp_status pp_context_launch_count(const pp_context *ctx, int64_t *n) {
 
 namespace pp {
 
-__global__ void __launch_bounds__(kBuildThreads) build_tables_kernel(BuildArgs a) {
+__global__ void __launch_bounds__(kBuildThreads, 8) build_tables_kernel(BuildArgs a) {
   const int b = blockIdx.x;
   if (b < a.node_blocks) {
     const int64_t gi = static_cast<int64_t>(b) * kBuildThreads + threadIdx.x;
@@ -168,10 +168,19 @@ __global__ void __launch_bounds__(kBuildThreads) build_tables_kernel(BuildArgs a
     return;
   }
   const int64_t eb = b - a.node_blocks;
+  // edge of this block: binary search over the edges' first blocks, staged
+  // in shared memory (independent loads instead of a chain of dependent ones)
+  constexpr int kStaged = 2048;
+  __shared__ int32_t first_blk[kStaged];
+  const bool staged = a.ne <= kStaged;
+  if (staged) {
+    for (int e = threadIdx.x; e < a.ne; e += kBuildThreads) first_blk[e] = static_cast<int32_t>(a.edges[e].blk_begin);
+    __syncthreads();
+  }
   int lo = 0, hi = a.ne - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (a.edges[mid].blk_begin <= eb)
+    if ((staged ? first_blk[mid] : a.edges[mid].blk_begin) <= eb)
       lo = mid;
     else
       hi = mid - 1;
