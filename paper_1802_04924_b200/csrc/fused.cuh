@@ -35,8 +35,12 @@ template <class T> struct FusedWave {
 };
 
 __device__ __forceinline__ int64_t first_item(int64_t rot) {
-  const int64_t g = gridDim.x;
-  return (static_cast<int64_t>(blockIdx.x) + g - rot % g) % g;
+  // (blockIdx + g - rot mod g) mod g, in 32-bit arithmetic when rot fits
+  // (a 64-bit remainder is ~70 instructions right after a barrier)
+  const unsigned g = gridDim.x;
+  const unsigned r = rot < (int64_t(1) << 32) ? static_cast<unsigned>(rot) % g : static_cast<unsigned>(rot % g);
+  const unsigned b = blockIdx.x >= r ? blockIdx.x - r : blockIdx.x + g - r;
+  return static_cast<int64_t>(b);
 }
 
 template <class T> struct FusedArgs {
@@ -76,6 +80,9 @@ constexpr int kFusedThreads = 256;
 // the co-resident CTA of a still-working SM does not have its L1 invalidated
 // on every poll.  `bar` must start with its low 31 bits zero (they return
 // there after every barrier).
+#ifndef PP_BARRIER_SLEEP_NS
+#define PP_BARRIER_SLEEP_NS 20
+#endif
 __device__ __forceinline__ void grid_barrier(unsigned int *bar, uint64_t *ts = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -88,7 +95,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int *bar, uint64_t *ts = n
     for (;;) {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
       if ((old ^ cur) & 0x80000000u) break;
-      __nanosleep(20);
+      __nanosleep(PP_BARRIER_SLEEP_NS);
     }
     if (ts) ts[4096] = global_ns();
     __threadfence(); // acquire: later reads see every CTA's writes
