@@ -248,9 +248,12 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
   using A = typename Acc<T>::type;
   for (int64_t vb = blockIdx.x; vb < a.nblk; vb += gridDim.x)
     enum_block<T>(a.en, a.k, a.ee, a.m, a.space, a.per_thread, static_cast<A *>(a.blk_val), a.blk_idx, vb);
+  // block 0's own DP items are done: it stages the finish lookups now
+  const bool staged = blockIdx.x == 0 && a.fin.smem_ok;
+  if (staged) finish_stage(a.fin, fused_smem);
   gsync();
   if (stamp) a.stamps[ph++] = global_ns();
-  if (blockIdx.x == 0) finish_block<T>(a.fin, fused_smem);
+  if (blockIdx.x == 0) finish_block<T>(a.fin, fused_smem, staged);
   if (stamp) a.stamps[ph++] = global_ns();
 }
 

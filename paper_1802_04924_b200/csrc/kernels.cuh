@@ -847,7 +847,8 @@ constexpr int kFinishThreads = 256;
 // independent and the CTA processes a wave in parallel (planner.hpp:309-319).
 // The cost terms are gathered in parallel, then summed by one thread in the
 // reference's order (cost.hpp:235-246) — bit-identical.
-template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a, unsigned char *smem = nullptr);
+template <class T>
+__device__ __forceinline__ void finish_block(const FinishArgs &a, unsigned char *smem = nullptr, bool staged = false);
 
 template <class T> __global__ void __launch_bounds__(kFinishThreads) finish_kernel(FinishArgs a) {
   finish_block<T>(a);
@@ -882,7 +883,20 @@ __host__ __device__ constexpr size_t finish_smem_bytes(int nl, int ne, int k) {
 // smem (optional): the fused kernel's dynamic region.  With it (a.smem_ok)
 // the static lookup arrays are staged up front and the unwind and re-sum
 // touch global memory only for the argmin and cost-table values.
-template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a, unsigned char *smem) {
+// Stages finish_block's lookup arrays into smem (independent loads, all in
+// flight at once).  The fused kernel runs it on block 0 before the barrier
+// that precedes the finish, off the critical path.
+__device__ __forceinline__ void finish_stage(const FinishArgs &a, unsigned char *smem) {
+  double *terms = reinterpret_cast<double *>(smem);
+  int64_t *co = reinterpret_cast<int64_t *>(terms + a.nl + a.ne), *xo = co + a.nl;
+  int32_t *ix = reinterpret_cast<int32_t *>(xo + a.ne), *cn = ix + a.nl, *es = cn + a.nl, *ed = es + a.ne;
+  int32_t *ncount = ed + a.ne;
+  for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) co[l] = a.cat_off[l], cn[l] = a.counts[l];
+  for (int e = threadIdx.x; e < a.ne; e += kFinishThreads) xo[e] = a.xoff[e], es[e] = a.esrc[e], ed[e] = a.edst[e];
+  for (int d = threadIdx.x; d < a.k; d += kFinishThreads) ncount[d] = a.nodes[d].count;
+}
+
+template <class T> __device__ __forceinline__ void finish_block(const FinishArgs &a, unsigned char *smem, bool staged) {
   using A = typename Acc<T>::type;
   const bool stamp = a.trace && threadIdx.x == 0;
   if (stamp) a.trace[0] = trace_ns();
@@ -892,13 +906,11 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
   int32_t *idx = a.indices;
   const int32_t *counts = a.counts, *esrc = a.esrc, *edst = a.edst;
   int32_t *ncount = nullptr;
-  if (sm) { // stage the lookup arrays (independent loads, all in flight at once)
+  if (sm) {
+    if (!staged) finish_stage(a, smem);
     int64_t *co = reinterpret_cast<int64_t *>(terms + a.nl + a.ne), *xo = co + a.nl;
     int32_t *ix = reinterpret_cast<int32_t *>(xo + a.ne), *cn = ix + a.nl, *es = cn + a.nl, *ed = es + a.ne;
     ncount = ed + a.ne;
-    for (int l = threadIdx.x; l < a.nl; l += kFinishThreads) co[l] = a.cat_off[l], cn[l] = a.counts[l];
-    for (int e = threadIdx.x; e < a.ne; e += kFinishThreads) xo[e] = a.xoff[e], es[e] = a.esrc[e], ed[e] = a.edst[e];
-    for (int d = threadIdx.x; d < a.k; d += kFinishThreads) ncount[d] = a.nodes[d].count;
     cat_off = co, xoff = xo, idx = ix, counts = cn, esrc = es, edst = ed;
   }
   __shared__ A sv[kFinishThreads / 32];
@@ -975,18 +987,22 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
     terms[a.nl + e] = ldexp(
         static_cast<double>(oxfer[xoff[e] + static_cast<int64_t>(idx[esrc[e]]) * counts[edst[e]] + idx[edst[e]]]), -a.shift);
   __syncthreads();
+  // zero-copy results (indices, digits, final cost) go to pinned host memory
+  // from threads 1.. while thread 0 re-sums the cost serially and writes it
+  const size_t cost_w = static_cast<size_t>(reinterpret_cast<const unsigned char *>(a.cost) - a.dev_res) / 4;
   if (threadIdx.x == 0) { // the reference's order: nodes by layer, then edges by id
     double t = 0.0;
     for (int x = 0; x < a.nl + a.ne; ++x) t += terms[x];
     *a.cost = t;
+    if (a.host_res) *reinterpret_cast<volatile double *>(a.host_res + 4 * cost_w) = t;
+  } else if (a.host_res) {
+    for (size_t b = threadIdx.x - 1; b < a.res_bytes / 4; b += kFinishThreads - 1)
+      if (b < cost_w || b >= cost_w + 2)
+        reinterpret_cast<volatile uint32_t *>(a.host_res)[b] = reinterpret_cast<const uint32_t *>(a.dev_res)[b];
   }
   if (stamp) a.trace[3] = trace_ns();
-  if (a.host_res) { // zero-copy: results straight into pinned host memory
-    __syncthreads();
-    for (size_t b = threadIdx.x; b < a.res_bytes / 4; b += kFinishThreads)
-      reinterpret_cast<volatile uint32_t *>(a.host_res)[b] = reinterpret_cast<const uint32_t *>(a.dev_res)[b];
-    __threadfence_system();
-  }
+  // no system fence: the host reads the block after synchronising with the
+  // kernel's completion, which orders these writes
   if (stamp) a.trace[4] = trace_ns();
 }
 
