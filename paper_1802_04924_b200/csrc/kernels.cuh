@@ -964,8 +964,18 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
       if (r.n == 0) {
         idx[r.removed] = r.am[at];
       } else {
+        // the path in batches: all loads of a batch in flight before its
+        // stores (idx may alias global memory, so a plain loop serialises)
         const uint16_t *pth = r.am + at * r.n;
-        for (int k = 0; k < r.n; ++k) idx[a.chain_nodes[r.removed + k]] = pth[k];
+        for (int k0 = 0; k0 < r.n; k0 += 8) {
+          int32_t node[8], val[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k0 + k < r.n) node[k] = a.chain_nodes[r.removed + k0 + k], val[k] = pth[k0 + k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k0 + k < r.n) idx[node[k]] = val[k];
+        }
       }
     }
     have = false;

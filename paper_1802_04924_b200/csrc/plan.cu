@@ -121,7 +121,7 @@ struct pp_prepared {
   int n_stamps = 0;
   size_t trace_off = 0; // PARPLAN_WAVE_TRACE: 8 stamps per wave (printed by pp_plan_profile)
   std::vector<char> phase_chain; // fused phases that are chain segments (profile kind 16)
-  int nblk_dbg = 0;
+  int nblk_dbg = 0, ngroups_dbg = 0;
   std::vector<double> fused_wave_work;
 
   ~pp_prepared() {
@@ -887,23 +887,50 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           im.final_gathers.emplace_back(amp(static_cast<int>(oi)), amfullp(static_cast<int>(oi)),
                                         static_cast<size_t>(blk(s.ops[oi].ne)) *
                                             cols[static_cast<size_t>(s.ops[oi].ne)] * 2);
-    // unwind records grouped by wave, last wave first (kernels.cuh finish_kernel)
+    // unwind records (kernels.cuh finish_block), visited last wave first and
+    // grouped by dependency level: a record's endpoints are final nodes
+    // (level 0) or removed by records of lower levels, so one group per
+    // level (the unwind's critical path) instead of one per wave
     std::vector<UnwindRec> recs;
-    std::vector<int32_t> groups{0};
-    for (int w = EWn; w >= 1; --w) {
-      for (int x = EWbegin[static_cast<size_t>(w)]; x < EWbegin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = EWexec[static_cast<size_t>(x)];
-        const Op &op = s.ops[static_cast<size_t>(oi)];
-        if (op.type) continue;
-        const int ch = chain_of_op[static_cast<size_t>(oi)];
-        if (ch < 0) {
-          recs.push_back(UnwindRec{amfullp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)], 0, 0});
-        } else if (chain_last_op[static_cast<size_t>(ch)] == oi) { // the whole chain, at its last fold
-          const ChainRec &cr = chain_recs[static_cast<size_t>(ch)];
-          recs.push_back(UnwindRec{cr.path, cr.node_off, op.u, op.v, cols[static_cast<size_t>(op.ne)], cr.n, 0});
+    std::vector<int> rlevel;
+    {
+      std::vector<int> lvl(static_cast<size_t>(t.nl), -1);
+      for (int d = 0; d < K; ++d) lvl[static_cast<size_t>(node_layer[static_cast<size_t>(d)])] = 0;
+      for (int w = EWn; w >= 1; --w) {
+        for (int x = EWbegin[static_cast<size_t>(w)]; x < EWbegin[static_cast<size_t>(w) + 1]; ++x) {
+          const int oi = EWexec[static_cast<size_t>(x)];
+          const Op &op = s.ops[static_cast<size_t>(oi)];
+          if (op.type) continue;
+          const int ch = chain_of_op[static_cast<size_t>(oi)];
+          if (ch >= 0 && chain_last_op[static_cast<size_t>(ch)] != oi) continue; // a chain: at its last fold
+          const int lu = lvl[static_cast<size_t>(op.u)], lv = lvl[static_cast<size_t>(op.v)];
+          PP_REQUIRE(lu >= 0 && lv >= 0, "unwind: record endpoint not yet assigned");
+          const int level = std::max(lu, lv) + 1;
+          if (ch < 0) {
+            recs.push_back(UnwindRec{amfullp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)], 0, 0});
+            lvl[static_cast<size_t>(op.removed)] = level;
+          } else {
+            const ChainRec &cr = chain_recs[static_cast<size_t>(ch)];
+            recs.push_back(UnwindRec{cr.path, cr.node_off, op.u, op.v, cols[static_cast<size_t>(op.ne)], cr.n, 0});
+            for (int k = 0; k < cr.n; ++k) lvl[static_cast<size_t>(chain_nodes[static_cast<size_t>(cr.node_off + k)])] = level;
+          }
+          rlevel.push_back(level);
         }
       }
-      if (static_cast<int32_t>(recs.size()) > groups.back()) groups.push_back(static_cast<int32_t>(recs.size()));
+    }
+    std::vector<int32_t> groups{0};
+    {
+      std::vector<size_t> order(recs.size());
+      for (size_t q = 0; q < order.size(); ++q) order[q] = q;
+      std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return rlevel[x] < rlevel[y]; });
+      std::vector<UnwindRec> sorted;
+      sorted.reserve(recs.size());
+      for (size_t q = 0; q < order.size(); ++q) {
+        if (q > 0 && rlevel[order[q]] != rlevel[order[q - 1]]) groups.push_back(static_cast<int32_t>(sorted.size()));
+        sorted.push_back(recs[order[q]]);
+      }
+      if (!sorted.empty()) groups.push_back(static_cast<int32_t>(sorted.size()));
+      recs.swap(sorted);
     }
     Packer &pk = im.pk;
     im.oG = pk.put(groups);
@@ -1156,6 +1183,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.blk_idx = bi;
     fa.nblk = nblk;
     P->nblk_dbg = nblk;
+    P->ngroups_dbg = im.nG;
     fa.nodes = en;
     fa.k = K;
     fa.node_layer = reinterpret_cast<const int32_t *>(dimg + im.oL);
@@ -1545,11 +1573,11 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
             }
           }
           const uint64_t *fr = &tr[static_cast<size_t>(16 * waves)];
-          std::fprintf(stderr, "finish: reduce %.0f unwind %.0f resum %.0f results %.0f ns (stage %.0f blk %.0f sync %.0f; nblk %d)\n",
+          std::fprintf(stderr, "finish: reduce %.0f unwind %.0f resum %.0f results %.0f ns (stage %.0f blk %.0f sync %.0f; nblk %d, unwind groups %d)\n",
                        static_cast<double>(fr[1] - fr[0]), static_cast<double>(fr[2] - fr[1]),
                        static_cast<double>(fr[3] - fr[2]), static_cast<double>(fr[4] - fr[3]),
                        static_cast<double>(fr[5] - fr[0]), static_cast<double>(fr[6] - fr[5]),
-                       static_cast<double>(fr[7] - fr[6]), P->nblk_dbg);
+                       static_cast<double>(fr[7] - fr[6]), P->nblk_dbg, P->ngroups_dbg);
         }
         for (int ph = 0; ph + 1 < P->n_stamps; ++ph) {
           const int pk = ph == 0       ? 11
