@@ -496,16 +496,22 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
     const int ng = min(wpr, nw); // groups that scanned anything
     for (int x = threadIdx.x; x < nr * nv; x += kFoldThreads) {
       const int r = x / nv, v = x - r * nv;
+      // (value, j) minimum over the groups as a tree (the order is
+      // irrelevant: ties resolve on the distinct j); groups past ng repeat
+      // group 0, which changes nothing
       T gvl[kChainGroups];
       int gjl[kChainGroups];
 #pragma unroll
-      for (int g = 0; g < kChainGroups; ++g)
-        if (g < ng) gvl[g] = gv[(g * c.rows + r) * kChainMax + v], gjl[g] = gj[(g * c.rows + r) * kChainMax + v];
+      for (int g = 0; g < kChainGroups; ++g) {
+        const int gg = g < ng ? g : 0;
+        gvl[g] = gv[(gg * c.rows + r) * kChainMax + v], gjl[g] = gj[(gg * c.rows + r) * kChainMax + v];
+      }
+#pragma unroll
+      for (int h = kChainGroups / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int g = 0; g < h; ++g) keep_min_v<T>(gvl[g + h], gjl[g + h], gvl[g], gjl[g]);
       T b = gvl[0];
       int j = gjl[0];
-#pragma unroll
-      for (int g = 1; g < kChainGroups; ++g)
-        if (g < ng) keep_min_v<T>(gvl[g], gjl[g], b, j);
       const int64_t o = static_cast<int64_t>(r0 + r) * nv + v;
       f.am[o] = static_cast<uint16_t>(j);
       if (c.path) amS[(k * c.rows + r) * kChainMax + v] = static_cast<uint16_t>(j);
