@@ -230,3 +230,28 @@ def test_evaluate_batch_matches_oracle(gpu, source):
         bad = ix.copy()
         bad[0, 0] = counts[0]
         t.evaluate_batch(bad)
+
+
+# fused-kernel knobs (read per prepare): every setting must give the oracle's
+# plan — the hand-rolled barrier vs grid.sync(), dynamic vs static build chunks,
+# chain segments and merge absorption off, the early table build off
+KNOBS = [{"PARPLAN_GRID_BARRIER": "0"}, {"PARPLAN_BUILD_DYNAMIC": "0"}, {"PARPLAN_CHAINS": "0"},
+         {"PARPLAN_MERGE_FUSE": "0"}, {"PARPLAN_EARLY_BUILD": "0"}, {"PARPLAN_STAGE": "0", "PARPLAN_PANEL": "0"}]
+
+
+@pytest.mark.parametrize("knobs", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()))
+def test_fused_knobs_match_oracle(gpu, knobs, monkeypatch):
+    import paper_1802_04924_b200 as P
+
+    for name, value in knobs.items():
+        monkeypatch.setenv(name, value)
+    for model, D in [("alexnet", 4), ("vgg16", 16), ("inception_chain", 16)]:
+        g = P.builtin_model(model, 32)
+        want = O.Instance.builtin(model, 32, "port").build_tables(D).plan()
+        prep = P.PreparedPlan(g, devices=P.DeviceGraph.uniform(D), ctx=gpu.ctx)
+        for _ in range(2):  # the counters and barrier words are rearmed by each launch
+            prep.launch()
+            r = prep.fetch()
+            assert list(r.indices) == list(want.indices) and r.cost == want.cost
+        r = P.plan(g, P.DeviceGraph.uniform(D), ctx=gpu.ctx)
+        assert list(r.indices) == list(want.indices) and r.cost == want.cost
