@@ -746,6 +746,24 @@ template <> struct Acc<int32_t> {
 constexpr int kEnumThreads = 256;
 constexpr int kMaxEnumNodes = 128;
 
+template <class A> __device__ __forceinline__ A shfl_xor_any(A v, int o) {
+  if constexpr (sizeof(A) == 8) {
+    long long x;
+    memcpy(&x, &v, 8);
+    x = __shfl_xor_sync(0xffffffffu, x, o);
+    memcpy(&v, &x, 8);
+    return v;
+  } else {
+    return __shfl_xor_sync(0xffffffffu, v, o);
+  }
+}
+
+// (value, linear index) order of the enumeration: lower value, then lower
+// index; INT64_MAX marks "no candidate".
+template <class A> __device__ __forceinline__ void keep_best(A ov, int64_t oi, A &bv, int64_t &bi) {
+  if (oi != INT64_MAX && (bi == INT64_MAX || ov < bv || (ov == bv && oi < bi))) bv = ov, bi = oi;
+}
+
 // Virtual block vb of the enumeration: kEnumThreads threads x per_thread
 // consecutive candidates each; writes the block's best to blk_val/blk_idx[vb].
 template <class T>
@@ -777,22 +795,22 @@ __device__ __forceinline__ void enum_block(const EnumNode *nodes, int k, const E
       }
     }
   }
-  __shared__ A sv[kEnumThreads];
-  __shared__ int64_t si[kEnumThreads];
-  sv[threadIdx.x] = best;
-  si[threadIdx.x] = bidx;
+  // (value, index) minimum: shuffles within each warp, then warp 0 over the
+  // warps' results (one barrier instead of one per tree level)
+  __shared__ A sv[kEnumThreads / 32];
+  __shared__ int64_t si[kEnumThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) keep_best<A>(shfl_xor_any<A>(best, o), __shfl_xor_sync(0xffffffffu, bidx, o), best, bidx);
+  if (lane == 0) sv[warp] = best, si[warp] = bidx;
   __syncthreads();
-  for (int s = kEnumThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const A ov = sv[threadIdx.x + s];
-      const int64_t oi = si[threadIdx.x + s];
-      if (oi != INT64_MAX &&
-          (si[threadIdx.x] == INT64_MAX || ov < sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])))
-        sv[threadIdx.x] = ov, si[threadIdx.x] = oi;
-    }
-    __syncthreads();
+  if (warp == 0) {
+    best = lane < kEnumThreads / 32 ? sv[lane] : A(0);
+    bidx = lane < kEnumThreads / 32 ? si[lane] : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) keep_best<A>(shfl_xor_any<A>(best, o), __shfl_xor_sync(0xffffffffu, bidx, o), best, bidx);
+    if (lane == 0) blk_val[vb] = best, blk_idx[vb] = bidx;
   }
-  if (threadIdx.x == 0) blk_val[vb] = sv[0], blk_idx[vb] = si[0];
   __syncthreads();
 }
 
@@ -860,23 +878,6 @@ template <class T> __global__ void __launch_bounds__(kFinishThreads) finish_kern
   finish_block<T>(a);
 }
 
-template <class A> __device__ __forceinline__ A shfl_xor_any(A v, int o) {
-  if constexpr (sizeof(A) == 8) {
-    long long x;
-    memcpy(&x, &v, 8);
-    x = __shfl_xor_sync(0xffffffffu, x, o);
-    memcpy(&v, &x, 8);
-    return v;
-  } else {
-    return __shfl_xor_sync(0xffffffffu, v, o);
-  }
-}
-
-// (value, linear index) order of the enumeration: lower value, then lower
-// index; INT64_MAX marks "no candidate".
-template <class A> __device__ __forceinline__ void keep_best(A ov, int64_t oi, A &bv, int64_t &bi) {
-  if (oi != INT64_MAX && (bi == INT64_MAX || ov < bv || (ov == bv && oi < bi))) bv = ov, bi = oi;
-}
 
 // Shared-memory layout of finish_block (when a.smem_ok): terms[nl + ne] |
 // cat_off[nl] | xoff[ne] (8-byte) | indices[nl] | counts[nl] | esrc[ne] |
