@@ -150,12 +150,20 @@ __global__ void __launch_bounds__(256) mp_pack_kernel(const MpFold *folds, int n
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5; // 32 x 8
   if (pb < static_cast<int64_t>(ti_a) * tj) {
     const int i0 = static_cast<int>(pb / tj) * 32, j0 = static_cast<int>(pb % tj) * 32;
-    for (int r = ty; r < 32; r += 8) { // row i = i0 + r, col j = j0 + tx
-      const int i = i0 + r, j = j0 + tx;
-      int v = kMpPad;
-      if (i < f.nu && j < f.nw) v = f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j] - f.ra[i];
-      tile[r][tx] = v;
-      if (i < f.nu) f.A16[static_cast<int64_t>(i) * f.nwp + j] = static_cast<uint16_t>(v);
+    // all four rows' loads first (the stores below could alias them as far
+    // as the compiler knows, which would serialise load -> store per row)
+    int v[4];
+    const int j = j0 + tx;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { // row i = i0 + ty + 8q, col j
+      const int i = i0 + ty + 8 * q;
+      v[q] = i < f.nu && j < f.nw ? f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j] - f.ra[i] : kMpPad;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = ty + 8 * q, i = i0 + r;
+      tile[r][tx] = v[q];
+      if (i < f.nu) f.A16[static_cast<int64_t>(i) * f.nwp + j] = static_cast<uint16_t>(v[q]);
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) { // A2T[j0 + r][i0 + tx]
@@ -168,12 +176,20 @@ __global__ void __launch_bounds__(256) mp_pack_kernel(const MpFold *folds, int n
   const int j0 = static_cast<int>(pb / tk) * 32, k0 = static_cast<int>(pb % tk) * 32;
   const int cbk = k0 + tx < f.nv ? mp_colmin(f, k0 + tx) : 0;
   if (j0 == 0 && ty == 0 && k0 + tx < f.nv) f.cb[k0 + tx] = cbk; // for mp_rescan
-  for (int r = ty; r < 32; r += 8) { // row j = j0 + r, col k = k0 + tx
-    const int j = j0 + r, k = k0 + tx;
-    int v = kMpPad;
-    if (j < f.nw && k < f.nv) v = f.t2[static_cast<int64_t>(j) * f.nv + k] - cbk;
-    tile[r][tx] = v;
-    f.B16[static_cast<int64_t>(j) * f.nvp + k] = static_cast<uint16_t>(v);
+  {
+    int v[4];
+    const int k = k0 + tx;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { // row j = j0 + ty + 8q, col k
+      const int j = j0 + ty + 8 * q;
+      v[q] = j < f.nw && k < f.nv ? f.t2[static_cast<int64_t>(j) * f.nv + k] - cbk : kMpPad;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = ty + 8 * q;
+      tile[r][tx] = v[q];
+      f.B16[static_cast<int64_t>(j0 + r) * f.nvp + k] = static_cast<uint16_t>(v[q]);
+    }
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8) { // B16T[k0 + r][j0 + tx]
