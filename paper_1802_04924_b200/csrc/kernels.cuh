@@ -324,6 +324,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// generic-proxy writes to GLOBAL memory (earlier phases of the same launch,
+// ordered by the grid barrier) before async-proxy (bulk copy) reads of them
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 // Copies the 16-byte-rounded byte range of [p, p + n) to dst; returns the
 // element offset of p inside dst.  (Device allocations are whole 256-byte
@@ -344,7 +347,9 @@ template <class T> __device__ __forceinline__ unsigned bulk_bytes(const T *p, in
 template <class T>
 __device__ __forceinline__ void chain_stage(const FoldDesc<T> &f, unsigned char *buf, size_t w_at, uint64_t *bar) {
   const int64_t n2 = static_cast<int64_t>(f.nw) * f.nv;
-  fence_proxy_async(); // earlier generic reads of buf happen before the async writes
+  // earlier generic reads of buf, and the generic stores that produced t2 / w
+  // (table build, earlier waves), happen before the async-proxy copies
+  fence_proxy_async_all();
   mbar_expect_tx(bar, bulk_bytes(f.t2, n2) + bulk_bytes(f.w, f.nw));
   bulk_range(reinterpret_cast<T *>(buf), f.t2, n2, bar);
   bulk_range(reinterpret_cast<T *>(buf + w_at), f.w, f.nw, bar);

@@ -1,31 +1,59 @@
-// minplus.cuh — the large-table Eq. 2 fold (K3) for exact fixed-point tables.
+// minplus.cuh — the large-table Eq. 2 fold (K3-U16) for exact fixed-point tables.
 //
 // out[i][k] = min_j (a[i][j] + b[j][k]),  a = w[j] + t1[i][j],  b = t2[j][k],
 // argmin = lowest j (planner.hpp:139-155), all in int32 units of 2^-s.
 //
 // Min-plus is shift-invariant per row of a and per column of b, so with
 // ra[i] = min_j a[i][j] and cb[k] = min_j b[j][k] the normalised operands
-// a' = a - ra, b' = b - cb lie in [0, rowspan(a)] x [0, colspan(b)].  When the
-// host's span bounds (propagated through the schedule) prove rowspan(a) <=
-// 16383 and colspan(b) <= 16382, every candidate a' + b' fits a signed 16-bit
-// lane with no overflow, and the fold runs two cells per instruction:
-// VIADDMNMX.S16x2 = min(a' + b', m) on a (cell, cell+1) pair — one
-// instruction per two (add, min) cell updates, i.e. the FP32 CUDA-core
-// roofline of one lane-op per cell (measured: tools/microbench).
+// a' = a - ra, b' = b - cb lie in [0, rowspan(a)] x [0, colspan(b)].  The host
+// propagates span bounds through the schedule and picks JB in {5, 4, 3} with
+//   ((rowspan(a) + colspan(b)) << JB) + 2^JB - 1 <= 65534,
+// so every candidate fits an unsigned 16-bit lane with its j carried along:
+//   a'' = (a' << JB) | (j mod 2^JB),   b'' = b' << JB,
+//   a'' + b'' = ((a' + b') << JB) | (j mod 2^JB).
+// The low bits never carry into the value, so a lane-wise u16 min over the
+// 2^JB candidates of one aligned j-group yields the minimum AND, among equal
+// values, the lowest j of the group.  VIADDMNMX.U16x2 = min(a'' + b'', m) on a
+// (cell, cell+1) pair is one instruction per two (add, min) cell updates — the
+// FP32 CUDA-core roofline of one lane-op per cell.  Across groups the kernel
+// keeps key = (value << (16 + JB) | group << JB | j-low) with an unsigned min:
+// smallest value first, then the lowest j.  So the exact value AND the exact
+// reference argmin come out of the fold itself:
+//   out = ra + cb + (key >> (16 + JB)),   am = key & 0xFFFF.
+// Padding: j >= nw has a'' = 0xFFFF, b'' = 0 (sum 0xFFFF above every real
+// candidate, no wrap); padded rows / columns are never stored.
 //
-// Argmin: per 32-j chunk the kernel keeps the chunk minimum and, with a strict
-// lane-wise "<" against the running best, the first chunk that attains the
-// final minimum (earlier chunks win ties).  A rescan of that chunk's 32
-// candidates — identical integer arithmetic — returns the first j with the
-// minimum value: exactly the reference's lowest-index tie-break.
+// Cap: with j0 the row minimum of b's column k (b'[j0][k] = 0), the fold's
+// minimum is at most a'[i][j0] <= rowspan(a), and likewise <= colspan(b); so
+// every minimum is <= M = min(rowspan bound, colspan bound).  Operands are
+// stored as min(x', M + 1): a candidate with a capped operand sums to > M and
+// can never be (or tie) the minimum, and every candidate equal to the minimum
+// keeps its exact operands.  So only 2(M + 1), not spanA + spanB, must fit:
+//   ((2M + 2) << JB) + 2^JB - 1 <= 65534.
 //
-//   mp_reduce  ra[i], cb[k]
-//   mp_pack    a' -> A2T [j][i] (u32, a' in both halves) and A16 [i][j];
-//              b' -> B16 [j][k] and B16T [k][j]  (s16), padded with 16383
-//   mp_fold    128x128 tile per CTA, 8x8 cells per thread, cp.async 4-stage
-//              pipeline over 32-j chunks; split-j across CTAs combine with
-//              atomicMin on (best << 16 | chunk)
-//   mp_rescan  first j of the winning chunk; out = ra + cb + best, am = j
+// The group key must order (value, group, j mod 2^JB): per group and cell
+// pair, one LOP3 moves the two j-low fields next to the group id
+// (gj = (m & LOW2) | G2) and one clears them from the values (mv = m & ~LOW2);
+// then per cell one PRMT builds (value << (16 + JB) | group << JB | j-low) and
+// one UMNMX keeps the minimum — 3 instructions per cell and group.
+//
+//   mp_minima  (once per plan) cb of every fold whose t2 is an original table,
+//              ra of every fold whose t1 is one
+//   mp_merge   Eq. 3 (out = t1 + t2) for merges whose output is a large
+//              fold's t2, with that fold's column minima (block min + atomicMin)
+//   mp_prep    (per wave) the operand blocks: a'' -> A [tile_i][chunk][32 j]
+//              [128 i] (u32, a'' in both halves), b'' -> B [tile_k][chunk]
+//              [32 j][128 k] (u16), each (tile, chunk) block contiguous (one
+//              bulk copy).  ra comes from the producing fold's epilogue when
+//              t1 is a fold output, else from a row pass here; cb likewise.
+//   mp_fold    persistent stream-K over (tile, 32-j chunk) units: 1 producer
+//              warp (cp.async.bulk -> 4-stage mbarrier ring) + 8 consumer warps
+//              (128x128 tile, 8x8 cells per thread).  A tile covered by one CTA
+//              is stored directly; a tile split between CTAs leaves its keys in
+//              the CTA's partial slot and the last CTA to arrive (per-tile
+//              counter) combines and stores it.  The epilogue also feeds the
+//              consuming large fold's row minima (out is its t1) or column
+//              minima (out is its t2) with warp-reduced atomicMin.
 #pragma once
 
 #include "kernels.cuh"
@@ -35,13 +63,18 @@
 
 namespace pp {
 
-constexpr int kMpTile = 128;   // output rows/cols per CTA
-constexpr int kMpChunk = 32;   // j per pipeline stage (and argmin chunk)
+constexpr int kMpTile = 128;                    // output rows/cols per tile
+constexpr int kMpChunk = 32;                    // j per pipeline stage
 constexpr int kMpStages = 4;
-constexpr int kMpThreads = 256;
-constexpr int kMpPad = 16383;  // padding value of a' and b'
-constexpr size_t kMpStageBytes = kMpChunk * kMpTile * 4 + kMpChunk * kMpTile * 2; // 24 KiB
-constexpr size_t kMpSmem = kMpStages * kMpStageBytes;                            // 96 KiB
+constexpr int kMpConsumers = 256;               // 8 warps
+constexpr int kMpThreads = kMpConsumers + 32;   // + 1 producer warp
+constexpr int kMpTileCells = kMpTile * kMpTile;
+constexpr unsigned kMpStageA = kMpChunk * kMpTile * 4; // 16 KiB
+constexpr unsigned kMpStageB = kMpChunk * kMpTile * 2; // 8 KiB
+constexpr unsigned kMpStageBytes = kMpStageA + kMpStageB;
+constexpr size_t kMpSmem = kMpStages * kMpStageBytes + 2 * kMpStages * 8 + 16;
+constexpr int kMpPrepRows = 32;  // rows per A-prep block
+constexpr int kMpPrepCols = 32;  // columns per B-prep block
 
 struct MpFold {
   // inputs (original or derived tables, int32 units)
@@ -51,22 +84,54 @@ struct MpFold {
   // outputs
   int32_t *out;  // [nu][nv]
   uint16_t *am;  // [nu][nv]
-  // scratch
-  int32_t *ra, *cb;   // [nu], [nv]
-  int32_t *cbp;       // [col_segs][nv] partial column minima (mp_reduce), folded into cb by mp_pack
-  int32_t col_segs;   // j segments of kMpRedColJ per column block
-  uint32_t *A2T;      // [nwp][nup]
-  uint16_t *A16;      // [nu][nwp]
-  uint16_t *B16;      // [nwp][nvp]
-  uint16_t *B16T;     // [nv][nwp]
-  int32_t *P;         // [nup][nvp] packed (best << 16 | chunk)
-  int32_t nu, nw, nv, nup, nwp, nvp;
-  int32_t tiles_i, tiles_k, splits, chunks_per_split;
-  int64_t fold_begin;   // first mp_fold block of this fold
-  int64_t red_begin;    // first mp_reduce block
-  int64_t pack_begin;   // first mp_pack block
-  int64_t rescan_begin; // first mp_rescan block
+  // row / column minima, order-preserving unsigned (x ^ 2^31); 0xFFFFFFFF
+  // before the producer's atomics (ready) or the prep pass
+  uint32_t *ra; // [nu]
+  uint32_t *cb; // [nv]
+  uint32_t *A;  // [tiles_i][nchunks][32][128]
+  uint16_t *B;  // [tiles_k][nchunks][32][128]
+  uint32_t *part; // [gridDim][2][128 * 128] stream-K partial keys (first / last segment of a CTA)
+  uint32_t *cnt;  // [tiles_i * tiles_k] arrivals, 0 at rest
+  // the large fold consuming `out` as its t1 (w_next, ra_next) or t2 (cb_next)
+  const int32_t *w_next;
+  uint32_t *ra_next, *cb_next;
+  int32_t nu, nw, nv, tiles_i, tiles_k, nchunks, jb;
+  int32_t cap; // operand cap M + 1
+  int32_t ra_ready, cb_ready; // minima supplied before mp_prep (epilogue / mp_colmin)
+  int32_t a_batches, b_batches; // mp_prep blocks per row group / column group (chunk batches)
+  int64_t prep_begin;   // first mp_prep block (A blocks, then B blocks)
+  int64_t colmin_begin; // first mp_minima column block (blocks only for an original t2)
+  int64_t rowmin_begin; // first mp_minima row block, counted after all column blocks (original t1)
+  int64_t unit_begin;   // first stream-K unit (tile-major, chunk fastest)
 };
+
+constexpr int kMpPrepBatch = 8; // chunks per mp_prep block when the minima are ready
+
+__host__ __device__ inline int64_t mp_prep_blocks(const MpFold &f) {
+  return static_cast<int64_t>((f.nu + kMpPrepRows - 1) / kMpPrepRows) * f.a_batches +
+         static_cast<int64_t>((f.nv + kMpPrepCols - 1) / kMpPrepCols) * f.b_batches;
+}
+
+__device__ __forceinline__ uint32_t mm_enc(int32_t x) { return static_cast<uint32_t>(x) ^ 0x80000000u; }
+__device__ __forceinline__ int32_t mm_dec(uint32_t x) { return static_cast<int32_t>(x ^ 0x80000000u); }
+
+// JB for a fold whose minima are <= M (operands capped at M + 1; 0: too wide)
+inline int mp_jbits(int64_t M) {
+  for (int jb = 5; jb >= 3; --jb)
+    if (((2 * M + 2) << jb) + (1 << jb) - 1 <= 65534) return jb;
+  return 0;
+}
+
+// Eq. 3 for a merge feeding a large fold's t2: out = a + b (planner.hpp:194-199,
+// one int32 add), plus that fold's column minima
+struct MpMerge {
+  const int32_t *a, *b;
+  int32_t *out;
+  uint32_t *cb; // consumer's column minima (encoded), 0xFF.. before
+  int32_t nr, nc;
+  int64_t blk_begin; // blocks: (32-column strip) x (64-row band)
+};
+constexpr int kMpMergeRows = 64;
 
 template <class F> __device__ __forceinline__ int find_desc(const MpFold *d, int n, int64_t b, F key) {
   int lo = 0, hi = n - 1;
@@ -80,21 +145,18 @@ template <class F> __device__ __forceinline__ int find_desc(const MpFold *d, int
   return lo;
 }
 
-// ---- mp_reduce: ra (one warp per row) and partial cb (32 columns x one
-// j segment per block: 8 warps x kMpRedColJ / 8 rows each, loads unrolled) --
-constexpr int kMpRedRowsPerBlock = 8; // 8 warps
-constexpr int kMpRedColJ = 128;       // j rows per column block
-__global__ void __launch_bounds__(256) mp_reduce_kernel(const MpFold *folds, int n) {
+// ---- mp_minima (once per plan): cb of folds whose t2 is an original table,
+// then ra of folds whose t1 is one (row blocks of 8 rows, one warp each) --------
+__global__ void __launch_bounds__(256) mp_minima_kernel(const MpFold *folds, int n, int64_t col_blocks) {
   const int64_t b = blockIdx.x;
-  const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.red_begin; })];
-  const int64_t rb = b - f.red_begin;
-  const int64_t row_blocks = (f.nu + kMpRedRowsPerBlock - 1) / kMpRedRowsPerBlock;
-  if (rb < row_blocks) {
-    const int i = static_cast<int>(rb) * kMpRedRowsPerBlock + (threadIdx.x >> 5);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (b >= col_blocks) {
+    const int64_t rb = b - col_blocks;
+    const MpFold &f = folds[find_desc(folds, n, rb, [](const MpFold &x) { return x.rowmin_begin; })];
+    const int i = static_cast<int>(rb - f.rowmin_begin) * 8 + warp;
     if (i >= f.nu) return;
-    const int lane = threadIdx.x & 31;
-    int m = INT_MAX;
     const int32_t *row = f.t1 + static_cast<int64_t>(i) * f.nw;
+    int m = INT_MAX;
     int j = lane;
     for (; j + 96 < f.nw; j += 128) { // four independent loads in flight
       const int a0 = f.w[j] + row[j], a1 = f.w[j + 32] + row[j + 32];
@@ -104,236 +166,468 @@ __global__ void __launch_bounds__(256) mp_reduce_kernel(const MpFold *folds, int
     for (; j < f.nw; j += 32) m = min(m, f.w[j] + row[j]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) f.ra[i] = m;
+    if (lane == 0) f.ra[i] = mm_enc(m);
     return;
   }
-  // columns: block (column block, j segment); 8 j-lanes x kMpRedColJ / 8 rows
+  const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.colmin_begin; })];
+  const int k = static_cast<int>(b - f.colmin_begin) * 32 + lane;
   __shared__ int part[8][33];
-  const int64_t cbk = rb - row_blocks;
-  const int seg = static_cast<int>(cbk % f.col_segs);
-  const int kc = static_cast<int>(cbk / f.col_segs) * 32 + (threadIdx.x & 31), lane_j = threadIdx.x >> 5;
-  const int jend = min(f.nw, (seg + 1) * kMpRedColJ);
   int m = INT_MAX;
-  if (kc < f.nv) {
-    int j = seg * kMpRedColJ + lane_j;
-    for (; j + 24 < jend; j += 32) { // four independent loads in flight
-      const int a0 = f.t2[static_cast<int64_t>(j) * f.nv + kc], a1 = f.t2[static_cast<int64_t>(j + 8) * f.nv + kc];
-      const int a2 = f.t2[static_cast<int64_t>(j + 16) * f.nv + kc], a3 = f.t2[static_cast<int64_t>(j + 24) * f.nv + kc];
+  if (k < f.nv) {
+    int j = warp;
+    for (; j + 24 < f.nw; j += 32) { // four independent loads in flight
+      const int a0 = f.t2[static_cast<int64_t>(j) * f.nv + k], a1 = f.t2[static_cast<int64_t>(j + 8) * f.nv + k];
+      const int a2 = f.t2[static_cast<int64_t>(j + 16) * f.nv + k], a3 = f.t2[static_cast<int64_t>(j + 24) * f.nv + k];
       m = min(m, min(min(a0, a1), min(a2, a3)));
     }
-    for (; j < jend; j += 8) m = min(m, f.t2[static_cast<int64_t>(j) * f.nv + kc]);
+    for (; j < f.nw; j += 8) m = min(m, f.t2[static_cast<int64_t>(j) * f.nv + k]);
   }
-  part[lane_j][threadIdx.x & 31] = m;
+  part[warp][lane] = m;
   __syncthreads();
-  if (threadIdx.x < 32 && kc < f.nv) {
+  if (tid < 32 && k < f.nv) {
+    int r = part[0][tid];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) r = min(r, part[q][tid]);
+    f.cb[k] = mm_enc(r);
+  }
+}
+
+__global__ void __launch_bounds__(256) mp_merge_kernel(const MpMerge *ms, int n) {
+  const int64_t b = blockIdx.x;
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ms[mid].blk_begin <= b)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const MpMerge &m = ms[lo];
+  const int64_t lb = b - m.blk_begin;
+  const int strips = (m.nc + 31) / 32;
+  const int k = static_cast<int>(lb % strips) * 32 + (threadIdx.x & 31);
+  const int r0 = static_cast<int>(lb / strips) * kMpMergeRows, rl = threadIdx.x >> 5;
+  __shared__ int part[8][33];
+  int cm = INT_MAX;
+  if (k < m.nc) {
+    int v[kMpMergeRows / 8];
+#pragma unroll
+    for (int q = 0; q < kMpMergeRows / 8; ++q) { // all loads first
+      const int r = r0 + rl + 8 * q;
+      const int64_t o = static_cast<int64_t>(r) * m.nc + k;
+      v[q] = r < m.nr ? m.a[o] + m.b[o] : INT_MAX;
+    }
+#pragma unroll
+    for (int q = 0; q < kMpMergeRows / 8; ++q) {
+      const int r = r0 + rl + 8 * q;
+      if (r < m.nr) m.out[static_cast<int64_t>(r) * m.nc + k] = v[q];
+      cm = min(cm, v[q]);
+    }
+  }
+  part[rl][threadIdx.x & 31] = cm;
+  __syncthreads();
+  if (threadIdx.x < 32 && k < m.nc) {
     int r = part[0][threadIdx.x];
 #pragma unroll
     for (int q = 1; q < 8; ++q) r = min(r, part[q][threadIdx.x]);
-    f.cbp[static_cast<int64_t>(seg) * f.nv + kc] = r;
+    atomicMin(m.cb + k, mm_enc(r));
   }
 }
 
-// cb[k] = min over the column's segment minima
-__device__ __forceinline__ int mp_colmin(const MpFold &f, int k) {
-  int m = f.cbp[k];
-  for (int s = 1; s < f.col_segs; ++s) m = min(m, f.cbp[static_cast<int64_t>(s) * f.nv + k]);
-  return m;
-}
+// ---- mp_prep ------------------------------------------------------------------
+// A block (row group of kMpPrepRows, chunk batch): the row pass (one warp per
+// four rows) when ra is not ready, then per chunk a 32x32 tile of a'' through
+// shared memory into the transposed, duplicated A layout: 16-byte loads (eight
+// lanes per 128-byte row segment), kMpPrepBatch chunks' loads in flight, and
+// 16-byte stores of four rows.  B block (column group of kMpPrepCols, chunk
+// batch): the column pass when cb is not ready, then the shifted u16 values
+// (no transpose).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// ---- mp_pack: 32x32 tiles; A part over (i, j) then B part over (j, k) -------
-__global__ void __launch_bounds__(256) mp_pack_kernel(const MpFold *folds, int n) {
-  __shared__ int32_t tile[32][33];
+__global__ void __launch_bounds__(256) mp_prep_kernel(const MpFold *folds, int n) {
+  pdl_launch_dependents(); // the fold may be scheduled now; it waits for this grid in griddepcontrol.wait
   const int64_t b = blockIdx.x;
-  const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.pack_begin; })];
-  int64_t pb = b - f.pack_begin;
-  const int ti_a = f.nup / 32, tj = f.nwp / 32, tk = f.nvp / 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5; // 32 x 8
-  if (pb < static_cast<int64_t>(ti_a) * tj) {
-    const int i0 = static_cast<int>(pb / tj) * 32, j0 = static_cast<int>(pb % tj) * 32;
-    // all four rows' loads first (the stores below could alias them as far
-    // as the compiler knows, which would serialise load -> store per row)
-    int v[4];
-    const int j = j0 + tx;
+  const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.prep_begin; })];
+  int64_t pb = b - f.prep_begin;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jb = f.jb;
+  const uint32_t jmask = (1u << jb) - 1;
+  const int64_t a_blocks = static_cast<int64_t>((f.nu + kMpPrepRows - 1) / kMpPrepRows) * f.a_batches;
+  pdl_wait(); // t1 / ra / cb come from the previous wave
+  if (pb < a_blocks) {
+    __shared__ int ras[kMpPrepRows];
+    __shared__ uint32_t tr[kMpPrepBatch][kMpChunk][kMpPrepRows + 1];
+    const int i0 = static_cast<int>(pb / f.a_batches) * kMpPrepRows;
+    const int batch = static_cast<int>(pb % f.a_batches);
+    const int c0 = f.a_batches > 1 ? batch * kMpPrepBatch : 0, c1 = f.a_batches > 1 ? min(f.nchunks, c0 + kMpPrepBatch) : f.nchunks;
+    if (!f.ra_ready) { // a_batches == 1: the whole row here
+#pragma unroll 1
+      for (int rr = 0; rr < kMpPrepRows / 8; ++rr) {
+        const int r = warp * (kMpPrepRows / 8) + rr, i = i0 + r;
+        int m = INT_MAX;
+        if (i < f.nu) {
+          const int32_t *row = f.t1 + static_cast<int64_t>(i) * f.nw;
+          int j = lane;
+          for (; j + 96 < f.nw; j += 128) { // four independent loads in flight
+            const int a0 = f.w[j] + row[j], a1 = f.w[j + 32] + row[j + 32];
+            const int a2 = f.w[j + 64] + row[j + 64], a3 = f.w[j + 96] + row[j + 96];
+            m = min(m, min(min(a0, a1), min(a2, a3)));
+          }
+          for (; j < f.nw; j += 32) m = min(m, f.w[j] + row[j]);
+        }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) { // row i = i0 + ty + 8q, col j
-      const int i = i0 + ty + 8 * q;
-      v[q] = i < f.nu && j < f.nw ? f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j] - f.ra[i] : kMpPad;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = ty + 8 * q, i = i0 + r;
-      tile[r][tx] = v[q];
-      if (i < f.nu) f.A16[static_cast<int64_t>(i) * f.nwp + j] = static_cast<uint16_t>(v[q]);
+        for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) {
+          ras[r] = m;
+          if (i < f.nu) f.ra[i] = mm_enc(m);
+        }
+      }
+    } else if (tid < kMpPrepRows) {
+      ras[tid] = i0 + tid < f.nu ? mm_dec(f.ra[i0 + tid]) : 0;
     }
     __syncthreads();
-    for (int r = ty; r < 32; r += 8) { // A2T[j0 + r][i0 + tx]
-      const uint32_t v = static_cast<uint32_t>(tile[tx][r]) & 0xffffu;
-      f.A2T[static_cast<int64_t>(j0 + r) * f.nup + i0 + tx] = v | (v << 16);
+    const int ti = i0 / kMpTile, ii0 = i0 % kMpTile;
+    const int lr = tid >> 3, lj = (tid & 7) * 4; // load: row lr, columns lj..lj+3 of each chunk
+    const int sj = tid >> 3, sr = (tid & 7) * 4; // store: j sj, rows sr..sr+3
+    const int i = i0 + lr;
+    const int32_t *row = f.t1 + static_cast<int64_t>(i) * f.nw;
+    const bool vec = ((f.nw & 3) | (reinterpret_cast<uintptr_t>(f.t1) & 15) | (reinterpret_cast<uintptr_t>(f.w) & 15)) == 0;
+    const int rai = ras[lr];
+    for (int cb0 = c0; cb0 < c1; cb0 += kMpPrepBatch) {
+      const int nb = min(kMpPrepBatch, c1 - cb0);
+      int4 v[kMpPrepBatch], wv[kMpPrepBatch];
+      if (vec && i0 + kMpPrepRows <= f.nu && (cb0 + kMpPrepBatch) * kMpChunk <= f.nw) { // interior: all loads first
+#pragma unroll
+        for (int q = 0; q < kMpPrepBatch; ++q) {
+          const int j = (cb0 + q) * kMpChunk + lj;
+          v[q] = __ldg(reinterpret_cast<const int4 *>(row + j));
+          wv[q] = __ldg(reinterpret_cast<const int4 *>(f.w + j));
+        }
+      } else {
+#pragma unroll
+      for (int q = 0; q < kMpPrepBatch; ++q) {
+        const int j = (cb0 + q) * kMpChunk + lj;
+        v[q] = wv[q] = make_int4(0, 0, 0, 0);
+        if (q < nb && i < f.nu) {
+          if (vec && j + 3 < f.nw) {
+            v[q] = *reinterpret_cast<const int4 *>(row + j);
+            wv[q] = *reinterpret_cast<const int4 *>(f.w + j);
+          } else {
+            int *pv = &v[q].x, *pw = &wv[q].x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (j + e < f.nw) pv[e] = row[j + e], pw[e] = f.w[j + e];
+          }
+        }
+      }
+      }
+#pragma unroll
+      for (int q = 0; q < kMpPrepBatch; ++q) {
+        const int *pv = &v[q].x, *pw = &wv[q].x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = (cb0 + q) * kMpChunk + lj + e;
+          tr[q][lj + e][lr] = i >= f.nu ? 0u
+                              : j < f.nw ? (static_cast<uint32_t>(min(pw[e] + pv[e] - rai, f.cap)) << jb) |
+                                               (static_cast<uint32_t>(j) & jmask)
+                                         : 0xFFFFu;
+        }
+      }
+      __syncthreads();
+      for (int q = 0; q < nb; ++q) {
+        uint32_t x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = tr[q][sj][sr + e] * 0x10001u; // a'' in both halves
+        *reinterpret_cast<uint4 *>(f.A + (static_cast<int64_t>(ti) * f.nchunks + cb0 + q) * (kMpChunk * kMpTile) +
+                                   sj * kMpTile + ii0 + sr) = make_uint4(x[0], x[1], x[2], x[3]);
+      }
+      __syncthreads();
     }
     return;
   }
-  pb -= static_cast<int64_t>(ti_a) * tj;
-  const int j0 = static_cast<int>(pb / tk) * 32, k0 = static_cast<int>(pb % tk) * 32;
-  const int cbk = k0 + tx < f.nv ? mp_colmin(f, k0 + tx) : 0;
-  if (j0 == 0 && ty == 0 && k0 + tx < f.nv) f.cb[k0 + tx] = cbk; // for mp_rescan
-  {
-    int v[4];
-    const int k = k0 + tx;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { // row j = j0 + ty + 8q, col k
-      const int j = j0 + ty + 8 * q;
-      v[q] = j < f.nw && k < f.nv ? f.t2[static_cast<int64_t>(j) * f.nv + k] - cbk : kMpPad;
+  pb -= a_blocks;
+  __shared__ int part[8][kMpPrepCols + 1];
+  __shared__ int cbs[kMpPrepCols];
+  const int k0 = static_cast<int>(pb / f.b_batches) * kMpPrepCols;
+  const int batch = static_cast<int>(pb % f.b_batches);
+  const int c0 = f.b_batches > 1 ? batch * kMpPrepBatch : 0, c1 = f.b_batches > 1 ? min(f.nchunks, c0 + kMpPrepBatch) : f.nchunks;
+  if (!f.cb_ready) {
+    const int k = k0 + lane;
+    int m = INT_MAX;
+    if (k < f.nv) {
+      int j = warp;
+      for (; j + 24 < f.nw; j += 32) {
+        const int a0 = f.t2[static_cast<int64_t>(j) * f.nv + k], a1 = f.t2[static_cast<int64_t>(j + 8) * f.nv + k];
+        const int a2 = f.t2[static_cast<int64_t>(j + 16) * f.nv + k], a3 = f.t2[static_cast<int64_t>(j + 24) * f.nv + k];
+        m = min(m, min(min(a0, a1), min(a2, a3)));
+      }
+      for (; j < f.nw; j += 8) m = min(m, f.t2[static_cast<int64_t>(j) * f.nv + k]);
     }
+    part[warp][lane] = m;
+    __syncthreads();
+    if (tid < kMpPrepCols) {
+      int r = part[0][tid];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = ty + 8 * q;
-      tile[r][tx] = v[q];
-      f.B16[static_cast<int64_t>(j0 + r) * f.nvp + k] = static_cast<uint16_t>(v[q]);
+      for (int q = 1; q < 8; ++q) r = min(r, part[q][tid]);
+      cbs[tid] = r;
+      if (k0 + tid < f.nv) f.cb[k0 + tid] = mm_enc(r);
     }
+  } else if (tid < kMpPrepCols) {
+    cbs[tid] = k0 + tid < f.nv ? mm_dec(f.cb[k0 + tid]) : 0;
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) { // B16T[k0 + r][j0 + tx]
-    const int k = k0 + r;
-    if (k < f.nv) f.B16T[static_cast<int64_t>(k) * f.nwp + j0 + tx] = static_cast<uint16_t>(tile[tx][r]);
+  const int tk = k0 / kMpTile, kk0 = k0 % kMpTile;
+  const int sj = tid >> 3, kq = (tid & 7) * 4; // j sj, columns kq..kq+3
+  int cbq[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) cbq[e] = cbs[kq + e];
+  const bool bvec = ((f.nv & 3) | (reinterpret_cast<uintptr_t>(f.t2) & 15)) == 0;
+  for (int cb0 = c0; cb0 < c1; cb0 += kMpPrepBatch) {
+    const int nb = min(kMpPrepBatch, c1 - cb0);
+    uint32_t v[kMpPrepBatch][4];
+    if (bvec && k0 + kMpPrepCols <= f.nv && (cb0 + kMpPrepBatch) * kMpChunk <= f.nw) { // interior: 16-byte loads first
+      int4 x[kMpPrepBatch];
+#pragma unroll
+      for (int q = 0; q < kMpPrepBatch; ++q)
+        x[q] = __ldg(reinterpret_cast<const int4 *>(f.t2 + static_cast<int64_t>((cb0 + q) * kMpChunk + sj) * f.nv + k0 + kq));
+#pragma unroll
+      for (int q = 0; q < kMpPrepBatch; ++q) {
+        const int *px = &x[q].x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[q][e] = static_cast<uint32_t>(min(px[e] - cbq[e], f.cap)) << jb;
+      }
+    } else {
+#pragma unroll
+    for (int q = 0; q < kMpPrepBatch; ++q) {
+      const int j = (cb0 + q) * kMpChunk + sj;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int k = k0 + kq + e;
+        v[q][e] = q < nb && j < f.nw && k < f.nv
+                      ? static_cast<uint32_t>(min(f.t2[static_cast<int64_t>(j) * f.nv + k] - cbq[e], f.cap)) << jb : 0u;
+      }
+    }
+    }
+#pragma unroll
+    for (int q = 0; q < kMpPrepBatch; ++q)
+      if (q < nb)
+        *reinterpret_cast<uint2 *>(f.B + (static_cast<int64_t>(tk) * f.nchunks + cb0 + q) * (kMpChunk * kMpTile) +
+                                   sj * kMpTile + kk0 + kq) = make_uint2(v[q][0] | (v[q][1] << 16), v[q][2] | (v[q][3] << 16));
   }
 }
 
-// ---- mp_fold ----------------------------------------------------------------
+// ---- mp_fold ------------------------------------------------------------------
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-// cp_async_commit / cp_async_wait: kernels.cuh
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kMpConsumers) : "memory"); }
 
-__global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *folds, int n) {
-  extern __shared__ __align__(16) unsigned char mp_smem[];
-  const int64_t b = blockIdx.x;
-  const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.fold_begin; })];
-  int64_t lb = b - f.fold_begin;
-  const int tiles = f.tiles_i * f.tiles_k;
-  const int split = static_cast<int>(lb / tiles);
-  lb -= static_cast<int64_t>(split) * tiles;
-  const int i0 = static_cast<int>(lb / f.tiles_k) * kMpTile, k0 = static_cast<int>(lb % f.tiles_k) * kMpTile;
-  const int nchunks = f.nwp / kMpChunk;
-  const int c_begin = split * f.chunks_per_split;
-  const int c_end = min(nchunks, c_begin + f.chunks_per_split);
+// stream-K ranges: CTA b owns units [b * units / G, (b + 1) * units / G)
+__device__ __forceinline__ int64_t mp_first(int64_t b, int64_t units, int64_t G) { return b * units / G; }
+// the CTA owning unit u: the largest b with b * units / G <= u
+__device__ __forceinline__ int64_t mp_owner(int64_t u, int64_t units, int64_t G) { return ((u + 1) * G - 1) / units; }
+
+template <int JB>
+__global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *folds, int n, int64_t units) {
+  extern __shared__ __align__(128) unsigned char mp_smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(mp_smem + kMpStages * kMpStageBytes);
+  uint64_t *empty = full + kMpStages;
+  int *last_flag = reinterpret_cast<int *>(empty + kMpStages);
+  const int64_t G = gridDim.x;
+  const int64_t u_begin = mp_first(blockIdx.x, units, G), u_end = mp_first(blockIdx.x + 1, units, G);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
-
-  auto stageA = [&](int s) { return reinterpret_cast<uint32_t *>(mp_smem + s * kMpStageBytes); };
-  auto stageB = [&](int s) {
-    return reinterpret_cast<uint32_t *>(mp_smem + s * kMpStageBytes + kMpChunk * kMpTile * 4);
-  };
-  auto load = [&](int c, int s) {
-    const int j0 = c * kMpChunk;
-    uint32_t *As = stageA(s);
-    uint32_t *Bs = stageB(s);
+  pdl_launch_dependents(); // the next wave's kernels may be scheduled; they wait in griddepcontrol.wait
+  if (tid == 0) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) { // A: 32 rows x 512 B = 1024 x 16 B
-      const int e = tid + q * kMpThreads, r = e >> 5, c16 = e & 31;
-      cp_async16(As + r * kMpTile + c16 * 4, f.A2T + static_cast<int64_t>(j0 + r) * f.nup + i0 + c16 * 4);
+    for (int s = 0; s < kMpStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kMpConsumers / 32);
     }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) { // B: 32 rows x 256 B = 512 x 16 B
-      const int e = tid + q * kMpThreads, r = e >> 4, c16 = e & 15;
-      cp_async16(Bs + r * (kMpTile / 2) + c16 * 4, f.B16 + static_cast<int64_t>(j0 + r) * f.nvp + k0 + c16 * 8);
-    }
-  };
-
-  // per cell: packed (chunk minimum << 16 | chunk); an integer min keeps the
-  // smallest value and, among equal values, the earliest chunk
-  int32_t key[8][8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) key[r][c] = INT_MAX;
-
-  // prologue: stages 0..S-2
-#pragma unroll
-  for (int s = 0; s < kMpStages - 1; ++s) {
-    if (c_begin + s < c_end) load(c_begin + s, s);
-    cp_async_commit();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int c = c_begin; c < c_end; ++c) {
-    const int s = (c - c_begin) % kMpStages;
-    cp_async_wait<kMpStages - 2>();
-    __syncthreads();
-    { // prefetch chunk c + S - 1 into the stage freed last iteration
-      const int cn = c + kMpStages - 1;
-      if (cn < c_end) load(cn, (cn - c_begin) % kMpStages);
-      cp_async_commit();
+  pdl_wait(); // operand blocks / minima from mp_prep, counters from the previous fold
+  __syncthreads();
+
+  if (warp == kMpConsumers / 32) { // producer: one thread streams the CTA's units in order
+    if (lane == 0) {
+      int64_t seg_hi = -1;
+      const MpFold *f = nullptr;
+      int64_t nn = 0;
+      for (int64_t u = u_begin; u < u_end; ++u, ++nn) {
+        if (u >= seg_hi) {
+          const int fi = find_desc(folds, n, u, [](const MpFold &x) { return x.unit_begin; });
+          f = &folds[fi];
+          seg_hi = fi + 1 < n ? folds[fi + 1].unit_begin : units;
+        }
+        const int64_t local = u - f->unit_begin;
+        const int tile = static_cast<int>(local / f->nchunks), c = static_cast<int>(local % f->nchunks);
+        const int ti = tile / f->tiles_k, tk = tile % f->tiles_k;
+        const int s = static_cast<int>(nn % kMpStages);
+        const unsigned ph = static_cast<unsigned>(nn / kMpStages) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        unsigned char *st = mp_smem + s * kMpStageBytes;
+        mbar_expect_tx(&full[s], kMpStageBytes);
+        bulk_g2s(st, f->A + (static_cast<int64_t>(ti) * f->nchunks + c) * (kMpChunk * kMpTile), kMpStageA, &full[s]);
+        bulk_g2s(st + kMpStageA, f->B + (static_cast<int64_t>(tk) * f->nchunks + c) * (kMpChunk * kMpTile), kMpStageB,
+                 &full[s]);
+      }
     }
-    const uint32_t *As = stageA(s) + ty * 8;
-    const uint32_t *Bs = stageB(s) + tx * 4;
-    uint32_t m[8][4];
-#pragma unroll
-    for (int jj = 0; jj < kMpChunk; ++jj) {
-      uint32_t a[8], bb[4];
-      *reinterpret_cast<uint4 *>(&a[0]) = *reinterpret_cast<const uint4 *>(As + jj * kMpTile);
-      *reinterpret_cast<uint4 *>(&a[4]) = *reinterpret_cast<const uint4 *>(As + jj * kMpTile + 4);
-      *reinterpret_cast<uint4 *>(&bb[0]) = *reinterpret_cast<const uint4 *>(Bs + jj * (kMpTile / 2));
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          m[r][q] = jj == 0 ? __vadd2(a[r], bb[q]) : __viaddmin_s16x2(a[r], bb[q], m[r][q]);
-    }
-    const uint32_t cid = static_cast<uint32_t>(c);
+    return;
+  }
+
+  // consumers: thread (ty, tx) owns rows ty*8..+7, columns tx*8..+7 of the tile
+  const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
+  constexpr int G_PER_STAGE = kMpChunk >> JB; // argmin groups per stage
+  constexpr uint32_t LOW2 = ((1u << JB) - 1) * 0x10001u;
+  int64_t u = u_begin, nn = 0;
+  while (u < u_end) {
+    const int fi = find_desc(folds, n, u, [](const MpFold &x) { return x.unit_begin; });
+    const MpFold &f = folds[fi];
+    const int64_t local = u - f.unit_begin;
+    const int tile = static_cast<int>(local / f.nchunks);
+    const int c_first = static_cast<int>(local % f.nchunks);
+    const int64_t tile_lo = f.unit_begin + static_cast<int64_t>(tile) * f.nchunks, tile_hi = tile_lo + f.nchunks;
+    const int64_t seg_lo = u, seg_end = min(u_end, tile_hi);
+
+    // key = value << (16 + JB) | j (group << JB | j-low): lowest value, then lowest j
+    uint32_t key[8][8];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { // PRMT builds (half << 16 | chunk) for each half
-        key[r][2 * q] = min(key[r][2 * q], static_cast<int32_t>(__byte_perm(m[r][q], cid, 0x1054)));
-        key[r][2 * q + 1] = min(key[r][2 * q + 1], static_cast<int32_t>(__byte_perm(m[r][q], cid, 0x3254)));
+      for (int q = 0; q < 8; ++q) key[r][q] = 0xFFFFFFFFu;
+
+    for (int c = c_first; u < seg_end; ++u, ++nn, ++c) {
+      const int s = static_cast<int>(nn % kMpStages);
+      mbar_wait(&full[s], static_cast<unsigned>(nn / kMpStages) & 1u);
+      const uint32_t *As = reinterpret_cast<const uint32_t *>(mp_smem + s * kMpStageBytes) + ty * 8;
+      const uint32_t *Bs = reinterpret_cast<const uint32_t *>(mp_smem + s * kMpStageBytes + kMpStageA) + tx * 4;
+#pragma unroll
+      for (int g = 0; g < G_PER_STAGE; ++g) {
+        uint32_t m[8][4];
+#pragma unroll
+        for (int jj = g << JB; jj < (g + 1) << JB; ++jj) {
+          uint32_t a[8], bb[4];
+          *reinterpret_cast<uint4 *>(&a[0]) = *reinterpret_cast<const uint4 *>(As + jj * kMpTile);
+          *reinterpret_cast<uint4 *>(&a[4]) = *reinterpret_cast<const uint4 *>(As + jj * kMpTile + 4);
+          *reinterpret_cast<uint4 *>(&bb[0]) = *reinterpret_cast<const uint4 *>(Bs + jj * (kMpTile / 2));
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              m[r][q] = jj == (g << JB) ? __vadd2(a[r], bb[q]) : __viaddmin_u16x2(a[r], bb[q], m[r][q]);
+        }
+        const uint32_t G2 = static_cast<uint32_t>(c * G_PER_STAGE + g) * ((1u << JB) * 0x10001u); // group << JB, both halves
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t gj = (m[r][q] & LOW2) | G2, mv = m[r][q] & ~LOW2;
+            key[r][2 * q] = min(key[r][2 * q], __byte_perm(mv, gj, 0x1054));
+            key[r][2 * q + 1] = min(key[r][2 * q + 1], __byte_perm(mv, gj, 0x3276));
+          }
       }
-  }
-  cp_async_wait<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
 
-  // epilogue: packed (best << 16 | chunk), lexicographic min across splits
+    // ---- epilogue -----------------------------------------------------------
+    const int ti = tile / f.tiles_k, tk = tile % f.tiles_k;
+    const int i0 = ti * kMpTile + ty * 8, k0 = tk * kMpTile + tx * 8;
+    bool store = c_first == 0 && seg_end == tile_hi;
+    if (!store) { // split tile: partial keys to this CTA's slot; the last CTA to arrive combines
+      const int slot = seg_lo > tile_lo || u_begin == tile_lo ? 0 : 1; // the CTA's first segment: 0
+      uint32_t *mine = f.part + (static_cast<int64_t>(blockIdx.x) * 2 + slot) * kMpTileCells + (ty * 8) * kMpTile + tx * 8;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int i = i0 + ty * 8 + r;
-    int32_t *prow = f.P + static_cast<int64_t>(i) * f.nvp + k0 + tx * 8;
-    const int32_t *v = key[r];
-    if (f.splits == 1) {
-      *reinterpret_cast<int4 *>(prow) = *reinterpret_cast<const int4 *>(&v[0]);
-      *reinterpret_cast<int4 *>(prow + 4) = *reinterpret_cast<const int4 *>(&v[4]);
-    } else {
+      for (int r = 0; r < 8; ++r) {
+        *reinterpret_cast<uint4 *>(mine + r * kMpTile) = make_uint4(key[r][0], key[r][1], key[r][2], key[r][3]);
+        *reinterpret_cast<uint4 *>(mine + r * kMpTile + 4) = make_uint4(key[r][4], key[r][5], key[r][6], key[r][7]);
+      }
+      consumer_sync(); // the CTA's partial stores precede thread 0's release below
+      const int64_t b0 = mp_owner(tile_lo, units, G), b1 = mp_owner(tile_hi - 1, units, G);
+      if (tid == 0) {
+        __threadfence(); // release (cumulative over the CTA's stores)
+        const unsigned prev = atomicAdd(f.cnt + tile, 1u);
+        const bool last = prev + 1 == static_cast<unsigned>(b1 - b0 + 1);
+        if (last) {
+          __threadfence(); // acquire the other parts' stores
+          f.cnt[tile] = 0; // every part has arrived: restore for the next use
+        }
+        *last_flag = last;
+      }
+      consumer_sync();
+      store = *last_flag != 0;
+      consumer_sync(); // last_flag is rewritten by the next split tile
+      if (store) {
+        for (int64_t ob = b0; ob <= b1; ++ob) {
+          if (ob == blockIdx.x) continue;
+          const int oslot = mp_first(ob, units, G) >= tile_lo ? 0 : 1;
+          const uint32_t *other = f.part + (ob * 2 + oslot) * kMpTileCells + (ty * 8) * kMpTile + tx * 8;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) atomicMin(prow + q, v[q]);
+          for (int r = 0; r < 8; ++r) {
+            const uint4 lo = __ldcg(reinterpret_cast<const uint4 *>(other + r * kMpTile));
+            const uint4 hi = __ldcg(reinterpret_cast<const uint4 *>(other + r * kMpTile + 4));
+            key[r][0] = min(key[r][0], lo.x), key[r][1] = min(key[r][1], lo.y);
+            key[r][2] = min(key[r][2], lo.z), key[r][3] = min(key[r][3], lo.w);
+            key[r][4] = min(key[r][4], hi.x), key[r][5] = min(key[r][5], hi.y);
+            key[r][6] = min(key[r][6], hi.z), key[r][7] = min(key[r][7], hi.w);
+          }
+        }
+      }
+    }
+    if (store) {
+      int cbk[8], wn[8], cm[8]; // cm: the consumer's column minima over this thread's rows
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        cbk[q] = k0 + q < f.nv ? mm_dec(f.cb[k0 + q]) : 0;
+        wn[q] = f.ra_next && k0 + q < f.nv ? f.w_next[k0 + q] : 0;
+        cm[q] = INT_MAX;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r;
+        const bool row_ok = i < f.nu;
+        const int rai = row_ok ? mm_dec(f.ra[i]) : 0;
+        int32_t ov[8];
+        uint16_t av[8];
+        int nm = INT_MAX; // the consumer's row minimum over these columns
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          ov[q] = rai + cbk[q] + static_cast<int32_t>(key[r][q] >> (16 + JB));
+          av[q] = static_cast<uint16_t>(key[r][q] & 0xFFFFu);
+          if (k0 + q < f.nv) nm = min(nm, ov[q] + wn[q]);
+          if (row_ok) cm[q] = min(cm[q], ov[q]);
+        }
+        if (f.ra_next) { // 8 lanes share the row: reduce, one atomic per warp and row
+          nm = min(nm, __shfl_xor_sync(0xffffffffu, nm, 1));
+          nm = min(nm, __shfl_xor_sync(0xffffffffu, nm, 2));
+          nm = min(nm, __shfl_xor_sync(0xffffffffu, nm, 4));
+          if ((lane & 7) == 0 && row_ok && nm != INT_MAX) atomicMin(f.ra_next + i, mm_enc(nm));
+        }
+        if (!row_ok) continue;
+        int32_t *orow = f.out + static_cast<int64_t>(i) * f.nv + k0;
+        uint16_t *arow = f.am + static_cast<int64_t>(i) * f.nv + k0;
+        if (k0 + 8 <= f.nv && (f.nv & 7) == 0) {
+          *reinterpret_cast<int4 *>(orow) = *reinterpret_cast<const int4 *>(&ov[0]);
+          *reinterpret_cast<int4 *>(orow + 4) = *reinterpret_cast<const int4 *>(&ov[4]);
+          *reinterpret_cast<uint4 *>(arow) = *reinterpret_cast<const uint4 *>(&av[0]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (k0 + q < f.nv) orow[q] = ov[q], arow[q] = av[q];
+        }
+      }
+      if (f.cb_next) { // 4 lanes of a warp share each column: reduce, one atomic per warp and column
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          cm[q] = min(cm[q], __shfl_xor_sync(0xffffffffu, cm[q], 8));
+          cm[q] = min(cm[q], __shfl_xor_sync(0xffffffffu, cm[q], 16));
+          if (lane < 8 && k0 + q < f.nv && cm[q] != INT_MAX) atomicMin(f.cb_next + k0 + q, mm_enc(cm[q]));
+        }
+      }
     }
   }
-}
-
-// ---- mp_rescan: one thread per output cell ------------------------------------
-__global__ void __launch_bounds__(256) mp_rescan_kernel(const MpFold *folds, int n) {
-  const int64_t b = blockIdx.x;
-  const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.rescan_begin; })];
-  const int64_t cell = (b - f.rescan_begin) * 256 + threadIdx.x;
-  if (cell >= static_cast<int64_t>(f.nu) * f.nv) return;
-  const int i = static_cast<int>(cell / f.nv), k = static_cast<int>(cell % f.nv);
-  const int32_t p = f.P[static_cast<int64_t>(i) * f.nvp + k];
-  const int bestv = p >> 16, chunk = p & 0xffff;
-  const int j0 = chunk * kMpChunk;
-  const uint4 *ar = reinterpret_cast<const uint4 *>(f.A16 + static_cast<int64_t>(i) * f.nwp + j0);
-  const uint4 *br = reinterpret_cast<const uint4 *>(f.B16T + static_cast<int64_t>(k) * f.nwp + j0);
-  int jbest = j0 + kMpChunk; // sentinel
-#pragma unroll
-  for (int q = 3; q >= 0; --q) { // scan backwards so the first match wins without a branch
-    const uint4 av = ar[q], bv = br[q];
-    const uint32_t aw[4] = {av.x, av.y, av.z, av.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-    for (int e = 3; e >= 0; --e) {
-      const int hi = static_cast<int>(aw[e] >> 16) + static_cast<int>(bw[e] >> 16);
-      const int lo = static_cast<int>(aw[e] & 0xffffu) + static_cast<int>(bw[e] & 0xffffu);
-      const int j = j0 + q * 8 + e * 2;
-      if (hi == bestv) jbest = j + 1;
-      if (lo == bestv) jbest = j;
-    }
-  }
-  f.out[cell] = f.ra[i] + f.cb[k] + bestv;
-  f.am[cell] = static_cast<uint16_t>(jbest);
 }
 
 } // namespace pp

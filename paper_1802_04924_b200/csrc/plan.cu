@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 
 namespace pp {
 // tuning knobs read once per prepare (A/B experiments in one process)
@@ -303,15 +304,24 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // ---- large fixed-point folds: span certificate + per-wave scratch -----------
   // Span bounds per table (rows: max over rows of max-min; cols likewise),
   // propagated through the log: fold R(out) <= R(t2), K(out) <= K(t1);
-  // merge R = R1 + R2, K = K1 + K2.  A fold takes the S16x2 kernel when
-  // rowspan(w + t1) <= 16383 and colspan(t2) <= 16382 (minplus.cuh).
+  // merge R = R1 + R2, K = K1 + K2.  A fold takes the U16x2 kernel when
+  // rowspan(w + t1) + colspan(t2) leaves room for JB >= 3 argmin bits
+  // (minplus.cuh); a wave's folds share the smallest JB among them.
   std::vector<char> large(s.ops.size(), 0);
+  std::vector<int> fold_jb(s.ops.size(), 0);
   struct MpLayout {
-    size_t ra, cb, cbp, A2T, A16, B16, B16T, P;
-    int nup, nwp, nvp, splits, cps, segs;
+    size_t ra, cb, A, B, cnt; // A, B: per-wave section; cnt, ra, cb: persistent section
+    int nchunks, tiles_i, tiles_k;
   };
   std::vector<MpLayout> mpl(s.ops.size());
-  size_t mp_bytes = 0;
+  std::vector<int> wave_jb(static_cast<size_t>(s.n_waves) + 1, 0);
+  std::vector<int64_t> fold_m(s.ops.size(), 0);                    // bound on a fold's minima (cap - 1)
+  std::vector<int> mp_consumer(static_cast<size_t>(E_total), -1);  // large fold reading a table as t1
+  std::vector<int> mp_consumer2(static_cast<size_t>(E_total), -1); // large fold reading a table as t2
+  std::vector<int> mp_producer(static_cast<size_t>(E_total), -1); // large fold writing a table
+  std::vector<char> mp_merge_out(static_cast<size_t>(E_total), 0); // table written by an mp_merge
+  // persistent section: stream-K partial slots | counters (0 at rest) | ra, cb (0xFF.. before use)
+  size_t mp_bytes = 0, mp_part = 0, mp_cnt = 0, mp_ra = 0, mp_cb = 0;
   if constexpr (std::is_same_v<T, int32_t>) {
     std::vector<int64_t> R(static_cast<size_t>(E_total), 0), Kc(static_cast<size_t>(E_total), 0);
     for (int e = 0; e < t.ne; ++e) {
@@ -329,38 +339,28 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       R[o] = R[b2];
       Kc[o] = Kc[a];
       const int nu = rows[a], nw = t.counts[static_cast<size_t>(op.removed)], nv = cols[b2];
-      const int64_t spanA = t.node_span[static_cast<size_t>(op.removed)] + R[a], spanB = Kc[b2];
-      large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && spanA <= kMpPad && spanB <= kMpPad - 1 && !ctx->no_minplus;
+      // every minimum <= min(rowspan(w + t1), colspan(t2)) (minplus.cuh: cap)
+      fold_m[oi] = std::min(t.node_span[static_cast<size_t>(op.removed)] + R[a], Kc[b2]);
+      fold_jb[oi] = fold_m[oi] < 32768 ? mp_jbits(fold_m[oi]) : 0;
+      large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && fold_jb[oi] > 0 && !ctx->no_minplus;
+      if (large[oi] && nu_eff(op.e1) > 0) {
+        mp_consumer[a] = static_cast<int>(oi);
+        mp_consumer2[b2] = static_cast<int>(oi);
+        mp_producer[o] = static_cast<int>(oi);
+      }
     }
+    for (const Op &op : s.ops) // merges feeding a large fold's t2 run as mp_merge (with its column minima)
+      if (op.type && !shard && mp_consumer2[static_cast<size_t>(op.ne)] >= 0) mp_merge_out[static_cast<size_t>(op.ne)] = 1;
+    auto take = [&](size_t &at, size_t bytes) {
+      const size_t o = at;
+      at += align256(bytes);
+      return o;
+    };
+    // per wave: the operand blocks of its folds (reused by the next wave) and
+    // the tile counters (restored after every use, so shared by the waves)
     for (int w = 1; w <= s.n_waves; ++w) {
-      int64_t tiles = 0;
-      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = s.exec[static_cast<size_t>(x)];
-        if (!large[static_cast<size_t>(oi)]) continue;
-        const Op &op = s.ops[static_cast<size_t>(oi)];
-        tiles += static_cast<int64_t>((nu_eff(op.e1) + kMpTile - 1) / kMpTile) *
-                 ((cols[static_cast<size_t>(op.e2)] + kMpTile - 1) / kMpTile);
-      }
-      // split-j factor: minimise the makespan ceil(tiles * s / cap) / s of one
-      // launch (cap = co-resident mp_fold CTAs), with a small per-split cost
-      // for the packed-key atomics and the P initialisation
-      int64_t want = std::max<int64_t>(1, (2 * int64_t(ctx->sms) + tiles - 1) / std::max<int64_t>(1, tiles));
-      if (tiles > 0 && kn.mp_split_penalty_milli >= 0) {
-        want = 1;
-        static int mp_occ = 0;
-        if (!mp_occ) {
-          PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
-          PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mp_occ, mp_fold_kernel, kMpThreads, kMpSmem));
-          mp_occ = std::max(mp_occ, 1);
-        }
-        const double cap = static_cast<double>(ctx->sms) * mp_occ;
-        double best = 1e30;
-        for (int64_t sp = 1; sp <= 64; ++sp) {
-          const double cost = std::ceil(static_cast<double>(tiles * sp) / cap) / static_cast<double>(sp) + 0.001 * kn.mp_split_penalty_milli * sp;
-          if (cost < best - 1e-12) best = cost, want = sp;
-        }
-      }
-      size_t off = 0;
+      size_t off = 0, coff = 0;
+      int jb = 5;
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         if (!large[static_cast<size_t>(oi)]) continue;
@@ -369,39 +369,35 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)],
                   nv = cols[static_cast<size_t>(op.e2)];
         if (nu == 0) continue; // no rows of this fold on this rank
-        L.nup = (nu + kMpTile - 1) / kMpTile * kMpTile;
-        L.nvp = (nv + kMpTile - 1) / kMpTile * kMpTile;
-        L.nwp = (nw + kMpChunk - 1) / kMpChunk * kMpChunk;
-        const int nchunks = L.nwp / kMpChunk;
-        L.splits = static_cast<int>(std::min<int64_t>(want, nchunks));
-        L.cps = (nchunks + L.splits - 1) / L.splits;
-        L.splits = (nchunks + L.cps - 1) / L.cps;
-        auto take = [&](size_t bytes) {
-          const size_t o = off;
-          off += align256(bytes);
-          return o;
-        };
-        L.ra = take(static_cast<size_t>(nu) * 4);
-        L.cb = take(static_cast<size_t>(nv) * 4);
-        L.segs = (nw + kMpRedColJ - 1) / kMpRedColJ;
-        L.cbp = take(static_cast<size_t>(L.segs) * nv * 4);
-        L.A2T = take(static_cast<size_t>(L.nwp) * L.nup * 4);
-        L.A16 = take(static_cast<size_t>(nu) * L.nwp * 2);
-        L.B16 = take(static_cast<size_t>(L.nwp) * L.nvp * 2);
-        L.B16T = take(static_cast<size_t>(nv) * L.nwp * 2);
-        L.P = take(static_cast<size_t>(L.nup) * L.nvp * 4);
+        jb = std::min(jb, fold_jb[static_cast<size_t>(oi)]);
+        L.tiles_i = (nu + kMpTile - 1) / kMpTile;
+        L.tiles_k = (nv + kMpTile - 1) / kMpTile;
+        L.nchunks = (nw + kMpChunk - 1) / kMpChunk;
+        L.A = take(off, static_cast<size_t>(L.tiles_i) * L.nchunks * kMpStageA);
+        L.B = take(off, static_cast<size_t>(L.tiles_k) * L.nchunks * kMpStageB);
+        L.cnt = take(coff, static_cast<size_t>(L.tiles_i) * L.tiles_k * 4);
+        L.ra = take(mp_ra, static_cast<size_t>(nu) * 4);
+        L.cb = take(mp_cb, static_cast<size_t>(nv) * 4);
       }
+      wave_jb[static_cast<size_t>(w)] = jb;
       mp_bytes = std::max(mp_bytes, off);
+      mp_cnt = std::max(mp_cnt, coff);
     }
-    if (mp_bytes)
-      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(kMpSmem)));
+    if (mp_bytes) {
+      mp_part = static_cast<size_t>(ctx->sms) * 2 * kMpTileCells * 4;
+      // per device, every prepare (cheap; no process-wide cache across devices)
+      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
+      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
+      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
+    }
   }
+  const size_t mp_pbytes = mp_part + mp_cnt + mp_ra + mp_cb;
 
   const size_t tables_bytes =
       bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
   const size_t off_tables = 0, off_derived = tables_bytes, off_am = off_derived + align256(tab_plan.end()),
-               off_mp = off_am + align256(am_bytes), off_amfull = off_mp + align256(mp_bytes),
+               off_mp = off_am + align256(am_bytes), off_mpp = off_mp + align256(mp_bytes),
+               off_amfull = off_mpp + align256(mp_pbytes),
                off_gat = off_amfull + align256(amfull_bytes), off_image = off_gat + align256(gat_bytes);
 
   // ---- enumeration / unwind descriptors (pointer-free parts) ----------------
@@ -429,9 +425,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     double cells;
     size_t p0; // large folds: [p0, p0 + np) in mpf
     int np;
-    int64_t fold_blocks, red_blocks, pack_blocks, rescan_blocks;
+    int64_t units, prep_blocks; // large folds: stream-K units, mp_prep blocks
+    size_t mm0 = 0;             // min-plus merges: [mm0, mm0 + nmm) in mmv
+    int nmm = 0;
+    int64_t mm_blocks = 0;
     double mp_cells;
-    std::vector<std::pair<int32_t *, size_t>> p_init; // split folds: P <- 0x7f7f7f7f
+    int jb;
     std::vector<std::tuple<const void *, void *, size_t>> gathers; // sharded: derived t2 -> full, before the wave
   };
   struct Image {
@@ -447,6 +446,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<double> phase_work;  // cells per fused phase
     int nG;
     size_t res_bytes;
+    size_t oMM = 0;            // min-plus merges (all waves)
+    int n_mp = 0;              // large folds (all waves)
+    int64_t colmin_blocks = 0, rowmin_blocks = 0; // mp_minima blocks
   };
   const bool use_fused = mp_bytes == 0 && !ctx->no_fused && !shard;
   // ---- effective schedule of the fused kernel: merge absorption ------------
@@ -597,8 +599,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<FoldOps> fold_ops;
     std::vector<MergeDesc<T>> merges;
     std::vector<MpFold> mpf;
+    std::vector<MpMerge> mmv;
+    int64_t colmin_blocks = 0, rowmin_blocks = 0; // mp_minima blocks over all large folds (one launch per plan)
     for (int w = 1; w <= EWn; ++w) {
-      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, 0, 0, 0.0, {}, {}};
+      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, mmv.size(), 0, 0, 0.0, 0, {}};
       // a wave whose generic folds cover fewer than 2 x SMs 32x32 tiles uses
       // 16x16 tiles: 4x the blocks, a quarter of the per-tile latency
       int64_t big_tiles = 0;
@@ -640,39 +644,54 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         if constexpr (std::is_same_v<T, int32_t>) {
           if (large[static_cast<size_t>(oi)]) {
             const MpLayout &L = mpl[static_cast<size_t>(oi)];
-            unsigned char *sb = db + off_mp;
+            unsigned char *sb = db + off_mp, *pb = db + off_mpp;
+            auto rap = [&](int o) { return reinterpret_cast<uint32_t *>(pb + mp_part + mp_cnt + mpl[static_cast<size_t>(o)].ra); };
+            auto cbp = [&](int o) {
+              return reinterpret_cast<uint32_t *>(pb + mp_part + mp_cnt + mp_ra + mpl[static_cast<size_t>(o)].cb);
+            };
             MpFold f{};
             f.t1 = rowp(op.e1);
             f.t2 = t2p(op.e2);
             f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
             f.out = out;
             f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
-            f.ra = reinterpret_cast<int32_t *>(sb + L.ra);
-            f.cb = reinterpret_cast<int32_t *>(sb + L.cb);
-            f.cbp = reinterpret_cast<int32_t *>(sb + L.cbp);
-            f.col_segs = L.segs;
-            f.A2T = reinterpret_cast<uint32_t *>(sb + L.A2T);
-            f.A16 = reinterpret_cast<uint16_t *>(sb + L.A16);
-            f.B16 = reinterpret_cast<uint16_t *>(sb + L.B16);
-            f.B16T = reinterpret_cast<uint16_t *>(sb + L.B16T);
-            f.P = reinterpret_cast<int32_t *>(sb + L.P);
+            f.ra = rap(oi);
+            f.cb = cbp(oi);
+            f.A = reinterpret_cast<uint32_t *>(sb + L.A);
+            f.B = reinterpret_cast<uint16_t *>(sb + L.B);
+            f.part = reinterpret_cast<uint32_t *>(pb);
+            f.cnt = reinterpret_cast<uint32_t *>(pb + mp_part + L.cnt);
+            const int nxt = mp_consumer[static_cast<size_t>(op.ne)];
+            if (nxt >= 0) {
+              f.w_next = onode + t.cat_off[static_cast<size_t>(s.ops[static_cast<size_t>(nxt)].removed)];
+              f.ra_next = rap(nxt);
+            }
+            const int nxt2 = mp_consumer2[static_cast<size_t>(op.ne)];
+            if (nxt2 >= 0 && !shard) f.cb_next = cbp(nxt2); // row-sharded: a rank sees only its rows
+            f.ra_ready = op.e1 < t.ne || mp_producer[static_cast<size_t>(op.e1)] >= 0; // mp_minima / producer
+            // original t2: mp_colmin (once per plan); a large fold's or an mp_merge's output: their epilogues
+            f.cb_ready = op.e2 < t.ne || (!shard && (mp_producer[static_cast<size_t>(op.e2)] >= 0 ||
+                                                     mp_merge_out[static_cast<size_t>(op.e2)]));
+            f.cap = static_cast<int32_t>(fold_m[static_cast<size_t>(oi)] + 1);
             f.nu = nu_eff(op.e1);
             f.nw = t.counts[static_cast<size_t>(op.removed)];
             f.nv = cols[static_cast<size_t>(op.e2)];
-            f.nup = L.nup, f.nwp = L.nwp, f.nvp = L.nvp;
-            f.tiles_i = L.nup / kMpTile;
-            f.tiles_k = L.nvp / kMpTile;
-            f.splits = L.splits;
-            f.chunks_per_split = L.cps;
-            f.fold_begin = wr.fold_blocks;
-            wr.fold_blocks += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.splits;
-            f.red_begin = wr.red_blocks;
-            wr.red_blocks += (f.nu + kMpRedRowsPerBlock - 1) / kMpRedRowsPerBlock + static_cast<int64_t>((f.nv + 31) / 32) * L.segs;
-            f.pack_begin = wr.pack_blocks;
-            wr.pack_blocks += static_cast<int64_t>(f.nup / 32) * (f.nwp / 32) + static_cast<int64_t>(f.nwp / 32) * (f.nvp / 32);
-            f.rescan_begin = wr.rescan_blocks;
-            wr.rescan_blocks += (static_cast<int64_t>(f.nu) * f.nv + 255) / 256;
-            if (f.splits > 1) wr.p_init.push_back({f.P, static_cast<size_t>(L.nup) * L.nvp * 4});
+            f.tiles_i = L.tiles_i;
+            f.tiles_k = L.tiles_k;
+            f.nchunks = L.nchunks;
+            f.jb = wave_jb[static_cast<size_t>(s.ops[static_cast<size_t>(oi)].wave)];
+            const int batches = (f.nchunks + kMpPrepBatch - 1) / kMpPrepBatch;
+            f.a_batches = f.ra_ready ? batches : 1;
+            f.b_batches = f.cb_ready ? batches : 1;
+            f.prep_begin = wr.prep_blocks;
+            wr.prep_blocks += mp_prep_blocks(f);
+            f.colmin_begin = colmin_blocks;
+            if (op.e2 < t.ne) colmin_blocks += (f.nv + 31) / 32; // original t2 only (derived: producers)
+            f.rowmin_begin = rowmin_blocks;
+            if (op.e1 < t.ne) rowmin_blocks += (f.nu + 7) / 8;
+            f.unit_begin = wr.units;
+            wr.units += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.nchunks;
+            wr.jb = f.jb;
             wr.mp_cells += static_cast<double>(f.nu) * f.nw * f.nv;
             mpf.push_back(f);
             ++wr.np;
@@ -706,6 +725,25 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           folds.push_back(f);
           ++wr.nf;
         } else {
+          if constexpr (std::is_same_v<T, int32_t>) {
+            if (mp_merge_out[static_cast<size_t>(op.ne)]) { // feeds a large fold's t2: with its column minima
+              const int nxt2 = mp_consumer2[static_cast<size_t>(op.ne)];
+              MpMerge mm{};
+              mm.a = rowp(op.e1);
+              mm.b = rowp(op.e2);
+              mm.out = out;
+              mm.cb = reinterpret_cast<uint32_t *>(db + off_mpp + mp_part + mp_cnt + mp_ra +
+                                                   mpl[static_cast<size_t>(nxt2)].cb);
+              mm.nr = nu_eff(op.e1);
+              mm.nc = cols[static_cast<size_t>(op.ne)];
+              mm.blk_begin = wr.mm_blocks;
+              wr.mm_blocks += static_cast<int64_t>((mm.nc + 31) / 32) * ((mm.nr + kMpMergeRows - 1) / kMpMergeRows);
+              wr.cells += static_cast<double>(mm.nr) * mm.nc;
+              mmv.push_back(mm);
+              ++wr.nmm;
+              continue;
+            }
+          }
           MergeDesc<T> m;
           m.a = rowp(op.e1);
           m.b = rowp(op.e2);
@@ -747,7 +785,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<int> chain_last_op;
     std::vector<int32_t> chain_nodes;
     std::vector<int> chain_of_op(s.ops.size(), -1);
-    if (use_fused && kn.chains) {
+    // a segment has no grid barrier between its waves, so a later wave's
+    // output must never reuse a table an earlier chain item still reads:
+    // segments need every derived table kept (no liveness reuse)
+    if (use_fused && kn.chains && keep_all) {
       auto fits = [&](int w, int ws, size_t limit) {
         const WaveRange &wr = im.waves[static_cast<size_t>(w) - 1];
         if (wr.nm || wr.nf == 0) return false;
@@ -937,6 +978,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     im.nG = static_cast<int>(groups.size()) - 1;
     im.oT = scr(static_cast<size_t>(t.nl + t.ne) * sizeof(double));
     im.oMP = pk.put(mpf);
+    im.oMM = pk.put(mmv);
+    im.n_mp = static_cast<int>(mpf.size());
+    im.colmin_blocks = colmin_blocks;
+    im.rowmin_blocks = rowmin_blocks;
     im.oF = pk.put(folds);
     im.oM = pk.put(merges);
     { // per-phase work lists of the fused kernel (pointers into the sections above):
@@ -1107,46 +1152,88 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     P->step_work.push_back(static_cast<double>(t.ncells + t.xcells));
     ++launches;
   }
-  for (const auto &wr : im.waves) {
-    if (use_fused) break;
-    push_gathers(wr.gathers);
-    if (wr.np > 0) { // large fixed-point folds of this wave: reduce -> pack -> fold -> rescan
-      const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + wr.p0;
-      const int np = wr.np;
-      for (const auto &pi : wr.p_init) {
-        int32_t *pp = pi.first;
-        const size_t nb = pi.second;
-        P->steps.push_back([pp, nb](cudaStream_t st) { PP_CUDA(cudaMemsetAsync(pp, 0x7f, nb, st)); });
-        P->step_kind.push_back(5);
-        P->step_work.push_back(static_cast<double>(nb));
-      }
-      const int64_t rb = wr.red_blocks, pb = wr.pack_blocks, fb = wr.fold_blocks, sb = wr.rescan_blocks;
-      PP_REQUIRE(fb < (int64_t(1) << 31) && pb < (int64_t(1) << 31) && sb < (int64_t(1) << 31), "wave too large");
-      P->steps.push_back([ctx, mf, np, rb](cudaStream_t st) {
-        mp_reduce_kernel<<<static_cast<unsigned>(rb), 256, 0, st>>>(mf, np);
-        check_launch(ctx);
-      });
-      P->step_kind.push_back(6);
-      P->step_work.push_back(0.0);
-      P->steps.push_back([ctx, mf, np, pb](cudaStream_t st) {
-        mp_pack_kernel<<<static_cast<unsigned>(pb), 256, 0, st>>>(mf, np);
+  if (mp_pbytes) { // large folds: tile counters 0 at rest, row minima 0xFF.. before their producers
+    unsigned char *pz = db + off_mpp + mp_part;
+    const size_t nc_ = mp_cnt, nr_ = mp_ra + mp_cb;
+    P->steps.push_back([pz, nc_, nr_](cudaStream_t st) {
+      PP_CUDA(cudaMemsetAsync(pz, 0, nc_, st));
+      PP_CUDA(cudaMemsetAsync(pz + nc_, 0xFF, nr_, st));
+    });
+    P->step_kind.push_back(5);
+    P->step_work.push_back(static_cast<double>(nc_ + nr_));
+    if (im.colmin_blocks + im.rowmin_blocks > 0) {
+      const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP);
+      const int nmp = im.n_mp;
+      const int64_t cbk = im.colmin_blocks, all = im.colmin_blocks + im.rowmin_blocks;
+      PP_REQUIRE(all < (int64_t(1) << 31), "too many minima blocks");
+      P->steps.push_back([ctx, mf, nmp, cbk, all](cudaStream_t st) {
+        mp_minima_kernel<<<static_cast<unsigned>(all), 256, 0, st>>>(mf, nmp, cbk);
         check_launch(ctx);
       });
       P->step_kind.push_back(7);
       P->step_work.push_back(0.0);
-      P->steps.push_back([ctx, mf, np, fb](cudaStream_t st) {
-        mp_fold_kernel<<<static_cast<unsigned>(fb), kMpThreads, kMpSmem, st>>>(mf, np);
-        check_launch(ctx);
-      });
-      P->step_kind.push_back(8);
-      P->step_work.push_back(wr.mp_cells);
-      P->steps.push_back([ctx, mf, np, sb](cudaStream_t st) {
-        mp_rescan_kernel<<<static_cast<unsigned>(sb), 256, 0, st>>>(mf, np);
+      ++launches;
+    }
+  }
+  for (const auto &wr : im.waves) {
+    if (use_fused) break;
+    push_gathers(wr.gathers);
+    if (wr.nmm > 0) { // merges feeding large folds' t2 (independent of this wave's folds)
+      const MpMerge *mm = reinterpret_cast<const MpMerge *>(dimg + im.oMM) + wr.mm0;
+      const int nmm = wr.nmm;
+      const int64_t mb = wr.mm_blocks;
+      PP_REQUIRE(mb < (int64_t(1) << 31), "wave too large");
+      P->steps.push_back([ctx, mm, nmm, mb](cudaStream_t st) {
+        mp_merge_kernel<<<static_cast<unsigned>(mb), 256, 0, st>>>(mm, nmm);
         check_launch(ctx);
       });
       P->step_kind.push_back(9);
       P->step_work.push_back(0.0);
-      launches += 4;
+      ++launches;
+    }
+    if (wr.np > 0) { // large fixed-point folds of this wave: prep -> stream-K fold
+      const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + wr.p0;
+      const int np = wr.np;
+      const int64_t pb = wr.prep_blocks, units = wr.units;
+      PP_REQUIRE(pb < (int64_t(1) << 31), "wave too large");
+      const unsigned G = static_cast<unsigned>(std::min<int64_t>(units, int64_t(ctx->sms)));
+      const int jb = wr.jb;
+      // programmatic dependent launches: each kernel of the prep -> fold ->
+      // prep ... chain is scheduled while its predecessor drains and waits in
+      // griddepcontrol.wait (minplus.cuh) for its results
+      P->steps.push_back([ctx, mf, np, pb](cudaStream_t st) {
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(pb));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        PP_CUDA(cudaLaunchKernelEx(&cfg, mp_prep_kernel, mf, np));
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(6);
+      P->step_work.push_back(0.0);
+      P->steps.push_back([ctx, mf, np, units, G, jb](cudaStream_t st) {
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(kMpThreads);
+        cfg.dynamicSmemBytes = kMpSmem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        PP_CUDA(cudaLaunchKernelEx(&cfg, jb == 5 ? mp_fold_kernel<5> : jb == 4 ? mp_fold_kernel<4> : mp_fold_kernel<3>, mf,
+                                   np, units));
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(8);
+      P->step_work.push_back(wr.mp_cells);
+      launches += 2;
     }
     const int64_t grid = wr.ftiles + wr.mblocks;
     if (!grid) continue;
@@ -1253,7 +1340,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         // grow the dynamic allowance monotonically; keep the shared-memory
         // carveout at what two co-resident blocks need (the rest stays L1,
         // which the table build and the wave folds lean on)
-        static size_t dyn_set[2] = {0, 0};
+        // function attributes are per device: the allowance only ever grows,
+        // tracked per device under a lock (several contexts / threads)
+        static std::mutex mu;
+        static std::map<int, std::array<size_t, 2>> dev_set;
+        std::lock_guard<std::mutex> lock(mu);
+        size_t *dyn_set = dev_set[ctx->device].data();
         if (dyn_set[sizeof(T) == 8] < dyn) {
           PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
           cudaFuncAttributes fa_{};
@@ -1281,11 +1373,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       attr[1].val.clusterDim.x = static_cast<unsigned>(nc), attr[1].val.clusterDim.y = 1, attr[1].val.clusterDim.z = 1;
       int64_t cap = int64_t(ctx->sms) * per_sm;
       if (nc > 1) {
-        static bool attr_set[2] = {false, false};
-        if (!attr_set[sizeof(T) == 8]) {
-          PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-          attr_set[sizeof(T) == 8] = true;
-        }
+        PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cudaLaunchConfig_t q{};
         q.gridDim = dim3(static_cast<unsigned>(nc));
         q.blockDim = dim3(kFusedThreads);
