@@ -144,8 +144,12 @@ pp_status pp_context_create_on_stream(int32_t device, void *cuda_stream, pp_cont
 pp_status pp_context_stream(const pp_context *ctx, void **cuda_stream);
 pp_status pp_context_destroy(pp_context *ctx);
 pp_status pp_context_set_precision(pp_context *ctx, int32_t policy);
-/* 0 (default): large certified fixed-point folds use the S16x2 min-plus
- * kernel; 1: every fold uses the generic tiled kernel (for parity checks). */
+/* Bit mask.  0 (default): large certified fixed-point folds use the U16x2
+ * min-plus kernels (optimistic operand caps, checked on the device; a plan
+ * whose check fires is re-run with proven caps), plans without them one fused
+ * cooperative kernel.  Bit 0: every fold uses the generic tiled kernel (parity
+ * checks); bit 1: one launch per wave instead of the fused kernel; bit 2:
+ * proven min-plus operand caps only. */
 pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy);
 /* Multi-GPU: one process per GPU.  Rank 0 creates a 128-byte NCCL unique id,
  * the caller broadcasts it (e.g. torch.distributed), every rank attaches.  A

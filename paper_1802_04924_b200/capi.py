@@ -204,11 +204,12 @@ class Context:
         _check(lib().pp_context_set_precision(self.h, {"auto": 0, "fp64": 1}[precision]))
 
     def set_kernel_policy(self, policy: str) -> None:
-        """'auto': S16x2 min-plus for large certified folds, one fused cooperative kernel
-        for plans without them; 'generic': tiled fold only; 'unfused': one launch per
-        wave; 'generic_unfused': both."""
-        _check(lib().pp_context_set_kernel_policy(
-            self.h, {"auto": 0, "generic": 1, "unfused": 2, "generic_unfused": 3}[policy]))
+        """'auto': U16x2 min-plus for large certified folds (optimistic operand caps,
+        checked on the device), one fused cooperative kernel for plans without them;
+        'generic': tiled fold only; 'unfused': one launch per wave; 'conservative':
+        min-plus with proven caps only; '+'-joined combinations ('generic+unfused')."""
+        bits = {"auto": 0, "generic": 1, "unfused": 2, "generic_unfused": 3, "conservative": 4}
+        _check(lib().pp_context_set_kernel_policy(self.h, sum(bits[p] for p in policy.split("+"))))
 
     def attach_comm(self, nranks: int, rank: int, unique_id: bytes) -> None:
         """Join an NCCL communicator: plans on this context are row-sharded across ranks."""

@@ -107,6 +107,7 @@ struct pp_context {
   int precision = PP_PRECISION_AUTO;
   bool no_minplus = false; // kernel policy bit 0: generic tiled fold only (parity tests)
   bool no_fused = false;   // kernel policy bit 1: one launch per wave instead of the fused kernel
+  bool mp_conservative = false; // kernel policy bit 2: min-plus folds with proven operand caps only
   // multi-GPU (pp_context_attach_comm): plans are row-sharded across the ranks
   void *comm = nullptr; // ncclComm_t
   int nranks = 1, rank = 0;

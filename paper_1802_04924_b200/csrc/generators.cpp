@@ -8,6 +8,7 @@
 // {1,1,1,i+1}.  Host code: generation is part of fixture construction, and the
 // tables are uploaded to the device like any other CostTables.
 #include "internal.hpp"
+#include "tables.hpp"
 
 #include <random>
 
@@ -93,6 +94,17 @@ pp_status pp_random_instance(pp_context *ctx, uint64_t seed, int32_t node_count,
                              int32_t device_count, int32_t configs_override, pp_graph **graph, pp_tables **tables) {
   pp_graph *g = nullptr;
   pp::Instance inst;
+  if (configs_override > 0) // config 5: the same draw order, int32 units (k/64 -> k) streamed to the device
+    return guard([&] {
+      PP_REQUIRE(ctx && graph && tables, "null argument");
+      if (node_count < 1) throw parplan::InputError("random graph needs at least one node");
+      std::mt19937_64 rng(seed);
+      auto gp = std::make_unique<pp_graph>(pp::sp_topology(rng, node_count, bp));
+      *tables = pp::tables_fixed_streamed(ctx, gp->impl, configs_override, 6, 640, [&](int32_t *dst, size_t n) {
+        for (size_t k = 0; k < n; ++k) dst[k] = static_cast<int32_t>(rng() % 641);
+      });
+      *graph = gp.release();
+    });
   pp_status st = guard([&] {
     PP_REQUIRE(ctx && graph && tables, "null argument");
     inst = pp::make_instance(seed, node_count, max_configs, bp, device_count, configs_override);

@@ -23,13 +23,19 @@
 // Padding: j >= nw has a'' = 0xFFFF, b'' = 0 (sum 0xFFFF above every real
 // candidate, no wrap); padded rows / columns are never stored.
 //
-// Cap: with j0 the row minimum of b's column k (b'[j0][k] = 0), the fold's
-// minimum is at most a'[i][j0] <= rowspan(a), and likewise <= colspan(b); so
-// every minimum is <= M = min(rowspan bound, colspan bound).  Operands are
-// stored as min(x', M + 1): a candidate with a capped operand sums to > M and
-// can never be (or tie) the minimum, and every candidate equal to the minimum
-// keeps its exact operands.  So only 2(M + 1), not spanA + spanB, must fit:
-//   ((2M + 2) << JB) + 2^JB - 1 <= 65534.
+// Cap: operands are stored as min(x', cap).  If a cell's computed minimum m''
+// is < cap, its minimising candidates have uncapped operands, so m'' is the
+// true minimum (every true candidate >= its capped one >= m''), and a j
+// attains m'' after capping iff it does before (a capped candidate is
+// >= cap > m''): value and lowest-index argmin are exact.  With j0 the
+// minimum of b's column k (b'[j0][k] = 0) the true minimum is <= a'[i][j0] <=
+// rowspan(a), and likewise <= colspan(b), so cap = M + 1 with
+// M = min(rowspan bound, colspan bound) is always safe (proven); only 2 cap,
+// not spanA + spanB, must fit: (2 cap << JB) + 2^JB - 1 <= 65534.  Static
+// bounds on derived tables are loose, so a fold whose proven JB would be < 5
+// runs optimistically at JB = 5 with the largest JB-5 cap: the epilogue
+// checks m'' < cap for every stored cell and raises `ovf` otherwise, and the
+// host then re-runs the plan with the proven caps.
 //
 // The group key must order (value, group, j mod 2^JB): per group and cell
 // pair, one LOP3 moves the two j-low fields next to the group id
@@ -49,9 +55,9 @@
 //   mp_fold    persistent stream-K over (tile, 32-j chunk) units: 1 producer
 //              warp (cp.async.bulk -> 4-stage mbarrier ring) + 8 consumer warps
 //              (128x128 tile, 8x8 cells per thread).  A tile covered by one CTA
-//              is stored directly; a tile split between CTAs leaves its keys in
-//              the CTA's partial slot and the last CTA to arrive (per-tile
-//              counter) combines and stores it.  The epilogue also feeds the
+//              is stored directly; a tile split between CTAs is combined and
+//              stored by the CTA holding its first chunk, from the other
+//              CTAs' part slots (per-tile release counter).  The epilogue also feeds the
 //              consuming large fold's row minima (out is its t1) or column
 //              minima (out is its t2) with warp-reduced atomicMin.
 #pragma once
@@ -90,13 +96,14 @@ struct MpFold {
   uint32_t *cb; // [nv]
   uint32_t *A;  // [tiles_i][nchunks][32][128]
   uint16_t *B;  // [tiles_k][nchunks][32][128]
-  uint32_t *part; // [gridDim][2][128 * 128] stream-K partial keys (first / last segment of a CTA)
+  uint32_t *part; // [gridDim][128 * 128] stream-K part keys (a CTA's first segment, when split)
   uint32_t *cnt;  // [tiles_i * tiles_k] arrivals, 0 at rest
   // the large fold consuming `out` as its t1 (w_next, ra_next) or t2 (cb_next)
   const int32_t *w_next;
   uint32_t *ra_next, *cb_next;
   int32_t nu, nw, nv, tiles_i, tiles_k, nchunks, jb;
-  int32_t cap; // operand cap M + 1
+  int32_t cap;   // operand cap: M + 1 (proven), or the JB's largest when optimistic
+  uint32_t *ovf; // optimistic cap: set when a minimum reaches the cap (the host re-plans conservatively)
   int32_t ra_ready, cb_ready; // minima supplied before mp_prep (epilogue / mp_colmin)
   int32_t a_batches, b_batches; // mp_prep blocks per row group / column group (chunk batches)
   int64_t prep_begin;   // first mp_prep block (A blocks, then B blocks)
@@ -121,6 +128,8 @@ inline int mp_jbits(int64_t M) {
     if (((2 * M + 2) << jb) + (1 << jb) - 1 <= 65534) return jb;
   return 0;
 }
+// the largest cap JB bits allow
+inline int32_t mp_max_cap(int jb) { return static_cast<int32_t>((65534 - ((1 << jb) - 1)) >> (jb + 1)); }
 
 // Eq. 3 for a merge feeding a large fold's t2: out = a + b (planner.hpp:194-199,
 // one int32 add), plus that fold's column minima
@@ -434,7 +443,6 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
   extern __shared__ __align__(128) unsigned char mp_smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(mp_smem + kMpStages * kMpStageBytes);
   uint64_t *empty = full + kMpStages;
-  int *last_flag = reinterpret_cast<int *>(empty + kMpStages);
   const int64_t G = gridDim.x;
   const int64_t u_begin = mp_first(blockIdx.x, units, G), u_end = mp_first(blockIdx.x + 1, units, G);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -536,48 +544,55 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
     const int ti = tile / f.tiles_k, tk = tile % f.tiles_k;
     const int i0 = ti * kMpTile + ty * 8, k0 = tk * kMpTile + tx * 8;
     bool store = c_first == 0 && seg_end == tile_hi;
-    if (!store) { // split tile: partial keys to this CTA's slot; the last CTA to arrive combines
-      const int slot = seg_lo > tile_lo || u_begin == tile_lo ? 0 : 1; // the CTA's first segment: 0
-      uint32_t *mine = f.part + (static_cast<int64_t>(blockIdx.x) * 2 + slot) * kMpTileCells + (ty * 8) * kMpTile + tx * 8;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        *reinterpret_cast<uint4 *>(mine + r * kMpTile) = make_uint4(key[r][0], key[r][1], key[r][2], key[r][3]);
-        *reinterpret_cast<uint4 *>(mine + r * kMpTile + 4) = make_uint4(key[r][4], key[r][5], key[r][6], key[r][7]);
-      }
-      consumer_sync(); // the CTA's partial stores precede thread 0's release below
+    if (!store) {
+      // split tile.  Its owner is the CTA holding its first chunk: the tile is
+      // the owner's LAST segment, and every other part is a later CTA's FIRST
+      // segment, deposited early in that CTA's run; so the owner rarely waits.
+      // Parts: keys to the CTA's slot, then one release increment (no round
+      // trip on the consumers' path).  Owner: acquire the count, combine, store.
       const int64_t b0 = mp_owner(tile_lo, units, G), b1 = mp_owner(tile_hi - 1, units, G);
-      if (tid == 0) {
-        __threadfence(); // release (cumulative over the CTA's stores)
-        const unsigned prev = atomicAdd(f.cnt + tile, 1u);
-        const bool last = prev + 1 == static_cast<unsigned>(b1 - b0 + 1);
-        if (last) {
-          __threadfence(); // acquire the other parts' stores
-          f.cnt[tile] = 0; // every part has arrived: restore for the next use
+      if (seg_lo != tile_lo) {
+        uint32_t *mine = f.part + static_cast<int64_t>(blockIdx.x) * kMpTileCells + (ty * 8) * kMpTile + tx * 8;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          *reinterpret_cast<uint4 *>(mine + r * kMpTile) = make_uint4(key[r][0], key[r][1], key[r][2], key[r][3]);
+          *reinterpret_cast<uint4 *>(mine + r * kMpTile + 4) = make_uint4(key[r][4], key[r][5], key[r][6], key[r][7]);
         }
-        *last_flag = last;
+        consumer_sync(); // the CTA's part stores precede thread 0's release
+        if (tid == 0) {
+          __threadfence();
+          atomicAdd(f.cnt + tile, 1u);
+        }
+        continue;
+      }
+      if (tid == 0) {
+        const unsigned want = static_cast<unsigned>(b1 - b0);
+        unsigned got;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(f.cnt + tile) : "memory");
+          if (got >= want) break;
+          __nanosleep(64);
+        }
+        f.cnt[tile] = 0; // every part has arrived: restore for the next use
       }
       consumer_sync();
-      store = *last_flag != 0;
-      consumer_sync(); // last_flag is rewritten by the next split tile
-      if (store) {
-        for (int64_t ob = b0; ob <= b1; ++ob) {
-          if (ob == blockIdx.x) continue;
-          const int oslot = mp_first(ob, units, G) >= tile_lo ? 0 : 1;
-          const uint32_t *other = f.part + (ob * 2 + oslot) * kMpTileCells + (ty * 8) * kMpTile + tx * 8;
+      for (int64_t ob = b0 + 1; ob <= b1; ++ob) {
+        const uint32_t *other = f.part + ob * kMpTileCells + (ty * 8) * kMpTile + tx * 8;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const uint4 lo = __ldcg(reinterpret_cast<const uint4 *>(other + r * kMpTile));
-            const uint4 hi = __ldcg(reinterpret_cast<const uint4 *>(other + r * kMpTile + 4));
-            key[r][0] = min(key[r][0], lo.x), key[r][1] = min(key[r][1], lo.y);
-            key[r][2] = min(key[r][2], lo.z), key[r][3] = min(key[r][3], lo.w);
-            key[r][4] = min(key[r][4], hi.x), key[r][5] = min(key[r][5], hi.y);
-            key[r][6] = min(key[r][6], hi.z), key[r][7] = min(key[r][7], hi.w);
-          }
+        for (int r = 0; r < 8; ++r) {
+          const uint4 lo = __ldcg(reinterpret_cast<const uint4 *>(other + r * kMpTile));
+          const uint4 hi = __ldcg(reinterpret_cast<const uint4 *>(other + r * kMpTile + 4));
+          key[r][0] = min(key[r][0], lo.x), key[r][1] = min(key[r][1], lo.y);
+          key[r][2] = min(key[r][2], lo.z), key[r][3] = min(key[r][3], lo.w);
+          key[r][4] = min(key[r][4], hi.x), key[r][5] = min(key[r][5], hi.y);
+          key[r][6] = min(key[r][6], hi.z), key[r][7] = min(key[r][7], hi.w);
         }
       }
+      store = true;
     }
     if (store) {
       int cbk[8], wn[8], cm[8]; // cm: the consumer's column minima over this thread's rows
+      bool capped = false;      // a minimum reached the (optimistic) cap
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         cbk[q] = k0 + q < f.nv ? mm_dec(f.cb[k0 + q]) : 0;
@@ -594,7 +609,9 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
         int nm = INT_MAX; // the consumer's row minimum over these columns
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          ov[q] = rai + cbk[q] + static_cast<int32_t>(key[r][q] >> (16 + JB));
+          const int32_t best = static_cast<int32_t>(key[r][q] >> (16 + JB));
+          if (row_ok && k0 + q < f.nv && best >= f.cap) capped = true;
+          ov[q] = rai + cbk[q] + best;
           av[q] = static_cast<uint16_t>(key[r][q] & 0xFFFFu);
           if (k0 + q < f.nv) nm = min(nm, ov[q] + wn[q]);
           if (row_ok) cm[q] = min(cm[q], ov[q]);
@@ -618,6 +635,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
             if (k0 + q < f.nv) orow[q] = ov[q], arow[q] = av[q];
         }
       }
+      if (capped && f.ovf) atomicOr(f.ovf, 1u);
       if (f.cb_next) { // 4 lanes of a warp share each column: reduce, one atomic per warp and column
 #pragma unroll
         for (int q = 0; q < 8; ++q) {

@@ -108,7 +108,9 @@ struct pp_prepared {
   PinnedBuf hmem;
   unsigned char *dbase = nullptr, *hbase = nullptr;
   unsigned char *sbase = nullptr; // device-only scratch (kernel-written buffers)
-  size_t image_off = 0, image_bytes = 0, res_off = 0, res_bytes = 0, off_idx = 0, off_cost = 0;
+  size_t image_off = 0, image_bytes = 0, res_off = 0, res_bytes = 0, off_idx = 0, off_cost = 0, off_ovf = 0;
+  bool mp_conservative = false; // min-plus folds with proven caps only (after an optimistic overflow)
+  int k_bound = 8;
   std::vector<std::function<void(cudaStream_t)>> steps;
   int launches_per_run = 0;
   cudaGraph_t graph = nullptr;
@@ -314,8 +316,13 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     int nchunks, tiles_i, tiles_k;
   };
   std::vector<MpLayout> mpl(s.ops.size());
-  std::vector<int> wave_jb(static_cast<size_t>(s.n_waves) + 1, 0);
+  std::vector<std::vector<int>> wave_group_jb(static_cast<size_t>(s.n_waves) + 1); // JB per launch group
+  std::vector<int> mp_group(s.ops.size(), 0);
   std::vector<int64_t> fold_m(s.ops.size(), 0);                    // bound on a fold's minima (cap - 1)
+  std::vector<char> fold_opt(s.ops.size(), 0);                     // optimistic cap (checked on the device)
+  // proven caps only: after an optimistic run overflowed, on request, or
+  // row-sharded (every rank must take the same path)
+  const bool conservative = P->mp_conservative || ctx->mp_conservative || shard;
   std::vector<int> mp_consumer(static_cast<size_t>(E_total), -1);  // large fold reading a table as t1
   std::vector<int> mp_consumer2(static_cast<size_t>(E_total), -1); // large fold reading a table as t2
   std::vector<int> mp_producer(static_cast<size_t>(E_total), -1); // large fold writing a table
@@ -342,6 +349,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       // every minimum <= min(rowspan(w + t1), colspan(t2)) (minplus.cuh: cap)
       fold_m[oi] = std::min(t.node_span[static_cast<size_t>(op.removed)] + R[a], Kc[b2]);
       fold_jb[oi] = fold_m[oi] < 32768 ? mp_jbits(fold_m[oi]) : 0;
+      // optimistic JB 5 (cap checked in the epilogue) unless conservative
+      if (fold_jb[oi] < 5 && !conservative) fold_opt[oi] = 1, fold_jb[oi] = 5;
       large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && fold_jb[oi] > 0 && !ctx->no_minplus;
       if (large[oi] && nu_eff(op.e1) > 0) {
         mp_consumer[a] = static_cast<int>(oi);
@@ -356,11 +365,15 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       at += align256(bytes);
       return o;
     };
-    // per wave: the operand blocks of its folds (reused by the next wave) and
-    // the tile counters (restored after every use, so shared by the waves)
+    // per wave, in launch groups of at most kMpGroupBytes of operand blocks
+    // (a wide wave — 471 folds of config 5 — would need 45 GB at C = 4096):
+    // the operand blocks and tile counters (restored after every use) of one
+    // group are reused by the next group / wave
+    constexpr size_t kMpGroupBytes = size_t(2) << 30;
     for (int w = 1; w <= s.n_waves; ++w) {
       size_t off = 0, coff = 0;
-      int jb = 5;
+      int g = 0;
+      wave_group_jb[static_cast<size_t>(w)].assign(1, 5);
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         if (!large[static_cast<size_t>(oi)]) continue;
@@ -369,22 +382,32 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)],
                   nv = cols[static_cast<size_t>(op.e2)];
         if (nu == 0) continue; // no rows of this fold on this rank
-        jb = std::min(jb, fold_jb[static_cast<size_t>(oi)]);
         L.tiles_i = (nu + kMpTile - 1) / kMpTile;
         L.tiles_k = (nv + kMpTile - 1) / kMpTile;
         L.nchunks = (nw + kMpChunk - 1) / kMpChunk;
+        const size_t need = align256(static_cast<size_t>(L.tiles_i) * L.nchunks * kMpStageA) +
+                            align256(static_cast<size_t>(L.tiles_k) * L.nchunks * kMpStageB);
+        if (off > 0 && off + need > kMpGroupBytes) { // close the group
+          mp_bytes = std::max(mp_bytes, off);
+          mp_cnt = std::max(mp_cnt, coff);
+          off = coff = 0;
+          ++g;
+          wave_group_jb[static_cast<size_t>(w)].push_back(5);
+        }
+        mp_group[static_cast<size_t>(oi)] = g;
+        int &gjb = wave_group_jb[static_cast<size_t>(w)].back();
+        gjb = std::min(gjb, fold_jb[static_cast<size_t>(oi)]);
         L.A = take(off, static_cast<size_t>(L.tiles_i) * L.nchunks * kMpStageA);
         L.B = take(off, static_cast<size_t>(L.tiles_k) * L.nchunks * kMpStageB);
         L.cnt = take(coff, static_cast<size_t>(L.tiles_i) * L.tiles_k * 4);
         L.ra = take(mp_ra, static_cast<size_t>(nu) * 4);
         L.cb = take(mp_cb, static_cast<size_t>(nv) * 4);
       }
-      wave_jb[static_cast<size_t>(w)] = jb;
       mp_bytes = std::max(mp_bytes, off);
       mp_cnt = std::max(mp_cnt, coff);
     }
     if (mp_bytes) {
-      mp_part = static_cast<size_t>(ctx->sms) * 2 * kMpTileCells * 4;
+      mp_part = static_cast<size_t>(ctx->sms) * kMpTileCells * 4;
       // per device, every prepare (cheap; no process-wide cache across devices)
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
@@ -423,14 +446,17 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     int nf, nm;
     int64_t ftiles, mblocks;
     double cells;
-    size_t p0; // large folds: [p0, p0 + np) in mpf
-    int np;
-    int64_t units, prep_blocks; // large folds: stream-K units, mp_prep blocks
-    size_t mm0 = 0;             // min-plus merges: [mm0, mm0 + nmm) in mmv
+    struct MpGroup {
+      size_t p0 = 0; // large folds [p0, p0 + np) in mpf, one prep + fold launch pair
+      int np = 0;
+      int64_t units = 0, prep_blocks = 0; // stream-K units, mp_prep blocks
+      int jb = 5;
+      double cells = 0.0;
+    };
+    std::vector<MpGroup> mg;
+    size_t mm0 = 0; // min-plus merges: [mm0, mm0 + nmm) in mmv
     int nmm = 0;
     int64_t mm_blocks = 0;
-    double mp_cells;
-    int jb;
     std::vector<std::tuple<const void *, void *, size_t>> gathers; // sharded: derived t2 -> full, before the wave
   };
   struct Image {
@@ -439,6 +465,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<std::tuple<const void *, void *, size_t>> final_gathers; // sharded: final edges + argmins
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
     size_t oG, oT, oFW, oST, oTR, oCN; // oT, oST, oTR (+1), oBV, oBI: scratch offsets
+    size_t oOvf = 0;                   // min-plus optimistic-cap overflow flag (result slot)
     size_t scratch = 0;                // bytes of the scratch section
     int n_phases = 0;                // fused kernel: waves / chain segments
     size_t dyn_smem = 0;             // fused kernel dynamic shared memory
@@ -568,6 +595,14 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   auto make_image = [&](unsigned char *db, unsigned char *sb) {
     Image im;
     im.pk.bytes.reserve(ctx->last_image_bytes + 4096);
+    // result slots first, contiguous: indices[nl] | digits[K] | final_cost |
+    // cost | min-plus cap overflow flag
+    im.oRes = im.pk.put(std::vector<int32_t>(static_cast<size_t>(t.nl) + static_cast<size_t>(K) + 2));
+    im.oIdx = im.oRes;
+    im.oFC = im.pk.put(std::vector<double>(2));
+    im.oOvf = im.pk.put(std::vector<int32_t>(4));
+    im.res_bytes = im.oOvf + 16 - im.oRes;
+    auto ovf_ptr = [&] { return reinterpret_cast<uint32_t *>(db + off_image + im.oOvf); };
     auto scr = [&](size_t bytes) {
       const size_t off = im.scratch;
       im.scratch = off + align256(bytes);
@@ -602,7 +637,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<MpMerge> mmv;
     int64_t colmin_blocks = 0, rowmin_blocks = 0; // mp_minima blocks over all large folds (one launch per plan)
     for (int w = 1; w <= EWn; ++w) {
-      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, mpf.size(), 0, 0, 0, mmv.size(), 0, 0, 0.0, 0, {}};
+      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, {}, mmv.size(), 0, 0, {}};
       // a wave whose generic folds cover fewer than 2 x SMs 32x32 tiles uses
       // 16x16 tiles: 4x the blocks, a quarter of the per-tile latency
       int64_t big_tiles = 0;
@@ -672,29 +707,38 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             // original t2: mp_colmin (once per plan); a large fold's or an mp_merge's output: their epilogues
             f.cb_ready = op.e2 < t.ne || (!shard && (mp_producer[static_cast<size_t>(op.e2)] >= 0 ||
                                                      mp_merge_out[static_cast<size_t>(op.e2)]));
-            f.cap = static_cast<int32_t>(fold_m[static_cast<size_t>(oi)] + 1);
+            if (fold_opt[static_cast<size_t>(oi)]) {
+              f.cap = mp_max_cap(f.jb);
+              f.ovf = ovf_ptr();
+            } else {
+              f.cap = static_cast<int32_t>(fold_m[static_cast<size_t>(oi)] + 1);
+            }
             f.nu = nu_eff(op.e1);
             f.nw = t.counts[static_cast<size_t>(op.removed)];
             f.nv = cols[static_cast<size_t>(op.e2)];
             f.tiles_i = L.tiles_i;
             f.tiles_k = L.tiles_k;
             f.nchunks = L.nchunks;
-            f.jb = wave_jb[static_cast<size_t>(s.ops[static_cast<size_t>(oi)].wave)];
+            const int gi = mp_group[static_cast<size_t>(oi)];
+            if (static_cast<int>(wr.mg.size()) <= gi) wr.mg.resize(static_cast<size_t>(gi) + 1);
+            auto &G = wr.mg[static_cast<size_t>(gi)];
+            if (G.np == 0) G.p0 = mpf.size();
+            G.jb = wave_group_jb[static_cast<size_t>(s.ops[static_cast<size_t>(oi)].wave)][static_cast<size_t>(gi)];
+            f.jb = G.jb;
             const int batches = (f.nchunks + kMpPrepBatch - 1) / kMpPrepBatch;
             f.a_batches = f.ra_ready ? batches : 1;
             f.b_batches = f.cb_ready ? batches : 1;
-            f.prep_begin = wr.prep_blocks;
-            wr.prep_blocks += mp_prep_blocks(f);
+            f.prep_begin = G.prep_blocks;
+            G.prep_blocks += mp_prep_blocks(f);
             f.colmin_begin = colmin_blocks;
             if (op.e2 < t.ne) colmin_blocks += (f.nv + 31) / 32; // original t2 only (derived: producers)
             f.rowmin_begin = rowmin_blocks;
             if (op.e1 < t.ne) rowmin_blocks += (f.nu + 7) / 8;
-            f.unit_begin = wr.units;
-            wr.units += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.nchunks;
-            wr.jb = f.jb;
-            wr.mp_cells += static_cast<double>(f.nu) * f.nw * f.nv;
+            f.unit_begin = G.units;
+            G.units += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.nchunks;
+            G.cells += static_cast<double>(f.nu) * f.nw * f.nv;
             mpf.push_back(f);
-            ++wr.np;
+            ++G.np;
             continue;
           }
         }
@@ -1047,11 +1091,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     }
     im.oBV = scr(static_cast<size_t>(nblk) * sizeof(A));
     im.oBI = scr(static_cast<size_t>(nblk) * sizeof(int64_t));
-    // result slots, contiguous: indices[nl] | digits[K] | final_cost | cost
-    im.oRes = pk.put(std::vector<int32_t>(static_cast<size_t>(t.nl) + static_cast<size_t>(K) + 2));
-    im.oIdx = im.oRes;
-    im.oFC = pk.put(std::vector<double>(2));
-    im.res_bytes = im.oFC + 16 - im.oRes;
     return im;
   };
 
@@ -1101,6 +1140,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->res_bytes = im.res_bytes;
   P->off_idx = im.oIdx;
   P->off_cost = im.oFC;
+  P->off_ovf = im.oOvf;
 
   if (bp) { // tables live in the plan's memory
     t.node.view(db + off_tables, static_cast<size_t>(t.ncells));
@@ -1153,11 +1193,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ++launches;
   }
   if (mp_pbytes) { // large folds: tile counters 0 at rest, row minima 0xFF.. before their producers
-    unsigned char *pz = db + off_mpp + mp_part;
+    unsigned char *pz = db + off_mpp + mp_part, *ovf = dimg + im.oOvf;
     const size_t nc_ = mp_cnt, nr_ = mp_ra + mp_cb;
-    P->steps.push_back([pz, nc_, nr_](cudaStream_t st) {
+    P->steps.push_back([pz, nc_, nr_, ovf](cudaStream_t st) {
       PP_CUDA(cudaMemsetAsync(pz, 0, nc_, st));
       PP_CUDA(cudaMemsetAsync(pz + nc_, 0xFF, nr_, st));
+      PP_CUDA(cudaMemsetAsync(ovf, 0, 4, st));
     });
     P->step_kind.push_back(5);
     P->step_work.push_back(static_cast<double>(nc_ + nr_));
@@ -1191,13 +1232,13 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       P->step_work.push_back(0.0);
       ++launches;
     }
-    if (wr.np > 0) { // large fixed-point folds of this wave: prep -> stream-K fold
-      const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + wr.p0;
-      const int np = wr.np;
-      const int64_t pb = wr.prep_blocks, units = wr.units;
+    for (const auto &grp : wr.mg) { // large fixed-point folds of this wave, per launch group: prep -> stream-K fold
+      const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + grp.p0;
+      const int np = grp.np;
+      const int64_t pb = grp.prep_blocks, units = grp.units;
       PP_REQUIRE(pb < (int64_t(1) << 31), "wave too large");
       const unsigned G = static_cast<unsigned>(std::min<int64_t>(units, int64_t(ctx->sms)));
-      const int jb = wr.jb;
+      const int jb = grp.jb;
       // programmatic dependent launches: each kernel of the prep -> fold ->
       // prep ... chain is scheduled while its predecessor drains and waits in
       // griddepcontrol.wait (minplus.cuh) for its results
@@ -1232,7 +1273,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         check_launch(ctx);
       });
       P->step_kind.push_back(8);
-      P->step_work.push_back(wr.mp_cells);
+      P->step_work.push_back(grp.cells);
       launches += 2;
     }
     const int64_t grid = wr.ftiles + wr.mblocks;
@@ -1411,6 +1452,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
 }
 
 static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
+  P->k_bound = k_bound;
   BuildPlan bp;
   if (dev) {
     P->own_t = std::make_unique<Tables>();
@@ -1427,6 +1469,49 @@ static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
     build_steps<double>(P, dev ? &bp : nullptr, k_bound);
   else
     build_steps<int32_t>(P, dev ? &bp : nullptr, k_bound);
+}
+
+// captures the plan's device work as one CUDA graph, on a private stream
+// (the context stream may be the legacy default stream, which cannot
+// capture); the graph is launched on the context stream
+static void capture(pp_prepared *P) {
+  pp_context *ctx = P->ctx;
+  if (P->exec) cudaGraphExecDestroy(P->exec), P->exec = nullptr;
+  if (P->graph) cudaGraphDestroy(P->graph), P->graph = nullptr;
+  cudaStream_t cap = nullptr;
+  PP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  const int64_t l0 = ctx->launches;
+  cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    try {
+      for (auto &st : P->steps) st(cap);
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(cap, &dummy);
+      cudaStreamDestroy(cap);
+      throw;
+    }
+    e = cudaStreamEndCapture(cap, &P->graph);
+  }
+  ctx->launches = l0;
+  cudaStreamDestroy(cap);
+  PP_CUDA(e);
+  PP_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
+}
+
+static void launch(pp_prepared *P, bool upload);
+
+// An optimistic min-plus operand cap was reached (minplus.cuh): the plan is
+// rebuilt with proven caps and run again, so results stay exact.  Only
+// fixed-point tables reach the min-plus kernels, and those are given
+// (plan_with_tables), so no table build is repeated.
+static void rerun_conservative(pp_prepared *P) {
+  PP_CUDA(cudaEventSynchronize(P->ctx->ev1));
+  P->mp_conservative = true;
+  build_steps<int32_t>(P, nullptr, P->k_bound);
+  P->uploaded = false;
+  if (!P->transient) capture(P);
+  launch(P, true);
 }
 
 static void launch(pp_prepared *P, bool upload) {
@@ -1453,6 +1538,12 @@ static void fetch(pp_prepared *P, int32_t *indices, pp_plan_result *res) {
   PP_REQUIRE(P->launched, "plan was not launched");
   pp_context *ctx = P->ctx;
   PP_CUDA(cudaEventSynchronize(ctx->ev1));
+  uint32_t ovf = 0;
+  std::memcpy(&ovf, P->hbase + P->off_ovf, 4);
+  if (ovf && !P->mp_conservative && P->t->mode != kFP64) {
+    rerun_conservative(P);
+    PP_CUDA(cudaEventSynchronize(ctx->ev1));
+  }
   float ms = 0.f;
   PP_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   const unsigned char *h = P->hbase + P->res_off;
@@ -1527,28 +1618,7 @@ pp_status pp_plan_prepare(pp_context *ctx, const pp_graph *g, const pp_device_de
     P->transient = false;
     PP_CUDA(cudaSetDevice(ctx->device));
     prepare(P.get(), dev, k_bound);
-    // capture the device work as one CUDA graph, on a private stream (the
-    // context stream may be the legacy default stream, which cannot capture);
-    // the graph is launched on the context stream
-    cudaStream_t cap = nullptr;
-    PP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    const int64_t l0 = ctx->launches;
-    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-    if (e == cudaSuccess) {
-      try {
-        for (auto &st : P->steps) st(cap);
-      } catch (...) {
-        cudaGraph_t dummy;
-        cudaStreamEndCapture(cap, &dummy);
-        cudaStreamDestroy(cap);
-        throw;
-      }
-      e = cudaStreamEndCapture(cap, &P->graph);
-    }
-    ctx->launches = l0;
-    cudaStreamDestroy(cap);
-    PP_CUDA(e);
-    PP_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
+    capture(P.get());
     *out = P.release();
   });
 }

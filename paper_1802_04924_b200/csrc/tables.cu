@@ -14,6 +14,8 @@
 // operation order and rounding.
 #include "tables.hpp"
 
+#include <functional>
+
 #include <type_traits>
 #include "build.cuh"
 
@@ -139,9 +141,10 @@ pp_status pp_context_set_precision(pp_context *ctx, int32_t policy) {
 pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy) {
   return guard([&] {
     PP_REQUIRE(ctx, "null context");
-    PP_REQUIRE(policy >= 0 && policy <= 3, "unknown kernel policy");
+    PP_REQUIRE(policy >= 0 && policy <= 7, "unknown kernel policy");
     ctx->no_minplus = (policy & 1) != 0;
     ctx->no_fused = (policy & 2) != 0;
+    ctx->mp_conservative = (policy & 4) != 0;
   });
 }
 
@@ -521,6 +524,67 @@ pp_status pp_tables_upload(pp_context *ctx, const pp_graph *gh, const int32_t *c
     *out = tp.release();
   });
 }
+
+} // extern "C"
+
+namespace pp {
+// Fixed-point tables of C configs per layer whose values (in units of 2^-shift,
+// within [0, vmax]) come from a host generator in fill order (node cells by
+// layer, then xfer cells by edge id, row-major), streamed to the device
+// through a pinned buffer: no host copy of the whole table set.
+pp_tables *tables_fixed_streamed(pp_context *ctx, const Graph &g, int32_t C, int shift, int64_t vmax,
+                                 const std::function<void(int32_t *, size_t)> &gen) {
+  PP_REQUIRE(C >= 1 && C <= 65535, "configs must be in 1..65535");
+  auto tp = std::make_unique<pp_tables>();
+  Tables &t = tp->impl;
+  t.ctx = ctx;
+  init_layout(t, g, std::vector<int32_t>(static_cast<size_t>(g.nl), C));
+  t.configs.resize(static_cast<size_t>(4 * t.ncells));
+  for (int64_t k = 0; k < t.ncells; ++k) {
+    t.configs[static_cast<size_t>(4 * k)] = 1, t.configs[static_cast<size_t>(4 * k + 1)] = 1;
+    t.configs[static_cast<size_t>(4 * k + 2)] = 1, t.configs[static_cast<size_t>(4 * k + 3)] = k % C + 1;
+  }
+  t.mode = kFixed;
+  t.shift = shift;
+  t.node_span.assign(static_cast<size_t>(g.nl), vmax);
+  t.absmax_node.assign(static_cast<size_t>(g.nl), vmax);
+  t.row_span.assign(static_cast<size_t>(g.ne), vmax);
+  t.col_span.assign(static_cast<size_t>(g.ne), vmax);
+  t.absmax_edge.assign(static_cast<size_t>(g.ne), vmax);
+  PP_REQUIRE(static_cast<double>(vmax) * (g.nl + g.ne) < 2147483647.0, "tables too large for exact fixed point");
+  t.node32.alloc(static_cast<size_t>(t.ncells));
+  t.xfer32.alloc(static_cast<size_t>(t.xcells));
+  constexpr size_t kChunk = size_t(16) << 20; // cells per staging half
+  PinnedBuf stage;
+  int32_t *h = static_cast<int32_t *>(stage.ensure(2 * kChunk * 4));
+  cudaEvent_t done[2];
+  PP_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+  PP_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+  ctx->begin();
+  int half = 0;
+  auto stream_into = [&](int32_t *dst, int64_t n) {
+    for (int64_t o = 0; o < n; o += static_cast<int64_t>(kChunk)) {
+      const size_t m = static_cast<size_t>(std::min<int64_t>(static_cast<int64_t>(kChunk), n - o));
+      int32_t *hb = h + half * kChunk;
+      PP_CUDA(cudaEventSynchronize(done[half])); // the copy that last used this half is done
+      gen(hb, m);
+      PP_CUDA(cudaMemcpyAsync(dst + o, hb, m * 4, cudaMemcpyHostToDevice, ctx->stream));
+      PP_CUDA(cudaEventRecord(done[half], ctx->stream));
+      half ^= 1;
+    }
+  };
+  PP_CUDA(cudaEventRecord(done[0], ctx->stream));
+  PP_CUDA(cudaEventRecord(done[1], ctx->stream));
+  stream_into(t.node32.p, t.ncells);
+  stream_into(t.xfer32.p, t.xcells);
+  t.build_ms = ctx->end_ms();
+  cudaEventDestroy(done[0]);
+  cudaEventDestroy(done[1]);
+  return tp.release();
+}
+} // namespace pp
+
+extern "C" {
 
 pp_status pp_tables_synthetic(pp_context *ctx, const pp_graph *gh, int32_t C, uint64_t seed, pp_tables **out) {
   return guard([&] {

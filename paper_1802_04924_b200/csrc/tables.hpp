@@ -1,6 +1,8 @@
 // tables.hpp — device-resident cost tables (CostTables, cost.hpp:148-168).
 #pragma once
 
+#include <functional>
+
 #include "device.hpp"
 
 #include <cstdint>
@@ -96,6 +98,9 @@ bool certify_fixed_point(const std::vector<double> &node, const std::vector<int6
                          const std::vector<int32_t> &counts, const std::vector<int> &esrc,
                          const std::vector<int> &edst, int *shift);
 
+// fixed-C fixed-point tables streamed from a host generator (generators.cpp)
+pp_tables *tables_fixed_streamed(pp_context *ctx, const Graph &g, int32_t C, int shift, int64_t vmax,
+                                 const std::function<void(int32_t *, size_t)> &gen);
 void compute_spans_fixed(Tables &t, const std::vector<int32_t> &node_units, const std::vector<int32_t> &xfer_units);
 
 } // namespace pp

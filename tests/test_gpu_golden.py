@@ -1,7 +1,9 @@
 """CUDA path vs fixtures generated from the REAL reference (tests/golden/
 make_golden.py via oracle/_ref) — including the sizes the CPU oracle is too
 slow for in a test: Inception-chain(12)@64 (reference: ~2 min) and the
-config-5 synthetic graph at C=256 (reference: ~45 s)."""
+config-5 synthetic graph at C=256 (reference: ~45 s), C=512 (~5 min) and
+C=1024 (~43 min; tests/golden/make_golden_synth.py)."""
+import glob
 import hashlib
 import json
 import os
@@ -40,14 +42,18 @@ def test_builtin_golden(gpu, case):
     assert [r.final_graph_nodes, r.node_eliminations, r.edge_eliminations] == case["stats"]
     sched, _ = g.schedule()
     assert [list(s[:7]) for s in sched] == case["log"]
-    if sum(case["config_counts"]) < 5000:
-        rg = P.ReducedGraph(g, t)
-        rg.reduce()
-        am = [sha([rg.argmin(i).astype(np.int32)]) for i, rec in enumerate(rg.log()) if rec[0] == 0]
-        assert am == case["argmin_sha256"]
+    # every argmin table of the reduction, hashed per record (I64 included)
+    rg = P.ReducedGraph(g, t)
+    rg.reduce()
+    am = [sha([rg.argmin(i).astype(np.int32)]) for i, rec in enumerate(rg.log()) if rec[0] == 0]
+    assert am == case["argmin_sha256"]
 
 
-@pytest.mark.parametrize("case", GOLD["synthetic"], ids=lambda c: f"C{c['configs']}")
+SYNTH = GOLD["synthetic"] + [json.load(open(p)) for p in sorted(
+    glob.glob(os.path.join(os.path.dirname(__file__), "golden", "reference_synth_C*.json")))]
+
+
+@pytest.mark.parametrize("case", SYNTH, ids=lambda c: f"C{c['configs']}")
 def test_synthetic_golden(gpu, case):
     import paper_1802_04924_b200 as P
 

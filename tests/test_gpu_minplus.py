@@ -70,3 +70,35 @@ def test_synthetic_graph_fast_vs_generic(gpu, C):
     assert list(a.indices) == list(b.indices) and a.cost == b.cost
     prof = P.PreparedPlan(g, tables=tf, ctx=fast).profile()
     assert sum(w for k, _, w in prof if k == "mp_fold") > 0
+
+
+@pytest.mark.parametrize("policy", ["auto", "conservative"])
+def test_optimistic_cap_overflow_reruns_exactly(gpu, policy):
+    """Every fold minimum is 2000 units, above the optimistic JB-5 operand cap
+    (1022): the device check fires and the plan is re-run with the proven cap
+    (min(rowspan, colspan) + 1 = 2001, JB 4) — same result as the generic fold."""
+    import paper_1802_04924_b200 as P
+
+    n = 96
+    g = _chain(P, 3)
+    t1 = np.full((n, n), 2000 / 64.0)
+    t1[np.arange(n), np.arange(n)] = 0.0
+    t2 = np.full((n, n), 2000 / 64.0)
+    t2[(np.arange(n) + 1) % n, np.arange(n)] = 0.0
+    rng = np.random.default_rng(7)
+    node = [rng.integers(0, 64, n) / 64.0, np.zeros(n), rng.integers(0, 64, n) / 64.0]
+    cat = [np.tile([1, 1, 1, 1], (n, 1)) for _ in range(3)]
+    fast, slow = P.Context(0), P.Context(0)
+    fast.set_kernel_policy(policy)
+    slow.set_kernel_policy("generic")
+    tf = P.upload_cost_tables(g, cat, node, [t1, t2], fast)
+    ts = P.upload_cost_tables(g, cat, node, [t1, t2], slow)
+    assert "mp_fold" in [k for k, _, _ in P.PreparedPlan(g, tables=tf, ctx=fast).profile()]
+    b = P.plan_with_tables(g, ts)
+    for _ in range(2):  # one-shot, then prepared (graph) plans
+        a = P.plan_with_tables(g, tf)
+        assert list(a.indices) == list(b.indices) and a.cost == b.cost
+        pp = P.PreparedPlan(g, tables=tf, ctx=fast)
+        pp.launch()
+        c = pp.fetch()
+        assert list(c.indices) == list(b.indices) and c.cost == b.cost
