@@ -177,8 +177,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": v / PAPER_MS, "dtype": "f64", "data": "synthetic (builtin model, analytic tables)",
-        "config": {"workload": f"plan(inception_chain(12)@{D})" if model == "inception_chain" else args.workload,
-                   "model": model, "batch": batch, "devices": D},
+        "config": config_of(model, batch, D),
         "cpu_baseline": {"value": v, "unit": "ms", "cores": 1, "kind": kind,
                          "sample": f"{args.steps} full plan() calls (tables + DP) on 1 host core, single-threaded "
                                    f"reference compiled -O3 -DNDEBUG; nproc={os.cpu_count()}",
@@ -196,8 +195,252 @@ def run_reference(args):
 # our arm
 # ---------------------------------------------------------------------------
 
-def run_ours(args):
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+# real-model workloads reported beside the headline (BASELINE configs 1-4 + the
+# 13-module chain, the nearest to Inception-v3's 120 nodes)
+MODELS = [("inception_chain", 16), ("inception_chain", 64), ("inception_chain(13)", 16), ("vgg16", 16),
+          ("alexnet", 4), ("lenet5", 4)]
+
+
+def golden_builtin(model, D):
+    with open(os.path.join(GOLDEN, "reference_golden.json")) as f:
+        for c in json.load(f)["builtins"]:
+            if c["model"] == model and c["devices"] == D:
+                return c
+    return None
+
+
+def config_of(model, batch, D):
+    """The config dict both arms print (identical keys and values)."""
+    wl = f"plan(inception_chain(12)@{D})" if model == "inception_chain" else f"plan({model}@{D})"
+    return {"workload": wl, "model": model, "batch": batch, "devices": D}
+
+
+def time_prepared(P, prep, stream, flush, steps, warmup):
+    import torch
+
+    for _ in range(warmup):
+        flush.zero_()
+        prep.launch()
+        prep.fetch()
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        prep.launch()
+        s1.record(stream)
+        r = prep.fetch()
+        ms.append(s0.elapsed_time(s1))
+    return ms, r
+
+
+def model_sweep(P, ctx, stream, flush, args):
+    """Device ms (prepared plan, inputs resident) and e2e ms (pp_plan with host
+    buffers) per real-model workload, each checked against the reference golden
+    (indices + cost as hex-float; tests/golden/make_golden.py)."""
+    import torch
+
+    out = {}
+    for model, D in MODELS:
+        g = P.builtin_model(model, 32)
+        dev = P.DeviceGraph.uniform(D)
+        prep = P.PreparedPlan(g, devices=dev, ctx=ctx)
+        dms, r = time_prepared(P, prep, stream, flush, args.steps, args.warmup)
+        e2e = []
+        for k in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = P.plan(g, dev, ctx=ctx)
+            if k >= args.warmup:
+                e2e.append((time.perf_counter() - t0) * 1e3)
+        gold = golden_builtin(model, D)
+        ok = gold is not None and [int(x) for x in r.indices] == gold["indices"] and float(r.cost).hex() == gold["cost"] \
+            and [int(x) for x in res.indices] == gold["indices"] and float(res.cost).hex() == gold["cost"]
+        out[f"{model}@{D}"] = {
+            "layers": g.n_layers, "edges": g.n_edges, "device_ms": statistics.mean(dms),
+            "device_ms_median": statistics.median(dms), "e2e_ms": statistics.mean(e2e),
+            "e2e_ms_median": statistics.median(e2e), "cost": r.cost, "waves": r.waves,
+            "matches_reference": bool(ok),
+            "reference_cpu_s": gold.get("reference_cpu_s") if gold else None}
+        del prep
+    return out
+
+
+def dropin_latency(args):
+    """bin/plan_bench: parplan::plan(graph, DeviceGraph::uniform(D)) through the
+    drop-in C++ API with a fresh graph per call (acceptance C5's measurement)."""
+    exe = os.path.join(ROOT, "paper_1802_04924_b200", "bin", "plan_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "paper_1802_04924_b200/bin/plan_bench not built"}
+    try:
+        cp = subprocess.run([exe, str(max(args.steps, 10)), "3"], capture_output=True, text=True, timeout=600,
+                            env=dict(os.environ, PARPLAN_DEVICE=os.environ.get("LOCAL_RANK", "0")))
+        rows = [json.loads(x) for x in cp.stdout.splitlines() if x.startswith("{")]
+    except Exception as exc:
+        return {"unavailable": f"plan_bench failed: {exc}"}
+    out = {}
+    for r in rows:
+        out[f"{r['kind']}:{r['workload']}"] = {"median_ms": r["median_ms"], "mean_ms": r["mean_ms"], "cost": r["cost"]}
+    return out
+
+
+def table_build(P, ctx):
+    """K1/K2 standalone (pp_tables_build) at I64: partition pairs per second
+    (one (p, q) pair of the reference's transfer_profile walk,
+    cost.hpp:103-131 — Σ over xfer cells of total(c_src) * total(c_dst)) and
+    GB/s of the table bytes written (8 B per xfer cell, 24 B per node cell)."""
     import numpy as np
+
+    g = P.builtin_model("inception_chain", 32)
+    dev = P.DeviceGraph.uniform(64)
+    ms = []
+    t = None
+    for _ in range(6):
+        t = P.build_cost_tables(g, dev, ctx)
+        ms.append(t.build_ms)
+    cat = t.download()[0]
+    tot = [np.prod(np.asarray(c, np.int64).reshape(-1, 4), axis=1) for c in cat]
+    es, ed, _ = g.edges()
+    pairs = sum(float(tot[s].sum()) * float(tot[d].sum()) for s, d in zip(es, ed))
+    xcells = sum(len(tot[s]) * len(tot[d]) for s, d in zip(es, ed))
+    ncells = sum(len(x) for x in tot)
+    best = min(ms[1:])
+    bytes_ = 8.0 * xcells + 24.0 * ncells
+    return {"workload": "build_cost_tables(inception_chain(12)@64)", "kernel": "build_tables_kernel (K1 + K2)",
+            "ms": best, "ms_all": ms[1:], "partition_pairs": pairs, "pairs_per_s": pairs / (best * 1e-3),
+            "xfer_cells": xcells, "bytes_written": bytes_, "achieved_gbs": bytes_ / (best * 1e-3) / 1e9,
+            "hbm_peak_gbs": peaks().get("hbm_gbs"),
+            "note": "integer-issue bound (SURVEY §8(d)); GB/s reported as §8(d) asks, judged by pairs/s"}
+
+
+def committed_traffic(kernel):
+    """DRAM bytes (read + write) of one launch of `kernel` from the newest
+    committed ncu --set full summary under profiles/ (the roofline's traffic)."""
+    import csv
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_full_summary.csv")), reverse=True):
+        with open(path) as f:
+            rows = [r for r in csv.DictReader(f) if kernel in r["kernel"]]
+        if not rows:
+            continue
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        total = 0.0
+        for r in rows:
+            if r["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                total += float(r["value"]) * scale.get(r["unit"], 1.0)
+        return total, f"{os.path.basename(path)}: dram__bytes_read.sum + dram__bytes_write.sum of one captured launch"
+    return None, "no committed ncu --set full summary"
+
+
+def minplus_point(P, ctx, stream, C, runs, check):
+    """Config-5 synthetic graph (1000 layers, bp 0.3, seed 1), C configs per
+    layer, exact int32 fixed point.  C <= 1024: the reference's draw order
+    (host mt19937_64, oracle.hpp:121-185), checked against the REAL reference's
+    result (tests/golden/reference_synth_C{C}.json); larger C: the device
+    generator, checked against the generic int32 fold on the same tables."""
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    gold_path = os.path.join(GOLDEN, f"reference_synth_C{C}.json")
+    if C <= 1024 and os.path.exists(gold_path):
+        g, t = P.synthetic_instance(1, 1000, C, 0.3, ctx=ctx)
+        tables = "reference draw order (host mt19937_64, oracle.hpp:121-185)"
+    else:
+        g = P.series_parallel_graph(1, 1000, 0.3)
+        t = P.synthetic_cost_tables(g, C, seed=1, ctx=ctx)
+        tables = "device generator (splitmix64, values k/64, k in [0, 640])"
+    prep = P.PreparedPlan(g, tables=t, ctx=ctx)
+    prep.launch()
+    r = prep.fetch()
+    sched = g.schedule()[0]
+    folds = [rec for rec in sched if rec[0] == 0]
+    global_cells = float(C) ** 3 * len(folds)
+    merge_cells = float(C) ** 2 * (len(sched) - len(folds))
+    runs_ = [prep.profile() for _ in range(runs)]
+    plan_ms = []
+    for _ in range(3):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s0.record(stream)
+        prep.launch()
+        s1.record(stream)
+        prep.fetch()
+        plan_ms.append(s0.elapsed_time(s1))
+    plan_ms = min(plan_ms)
+    if world > 1:
+        from paper_1802_04924_b200 import distributed as PD
+
+        plan_ms = PD.max_over_ranks(plan_ms, device="cuda")
+    by_kind = {}
+    for run in runs_:
+        for kind, ms, _ in run:
+            by_kind[kind] = by_kind.get(kind, 0.0) + ms / len(runs_)
+    fold = [(ms, w) for run in runs_ for kind, ms, w in run if kind == "mp_fold"]
+    fold_ms = sum(ms for ms, _ in fold) / len(runs_)
+    cells = sum(w for _, w in fold) / len(runs_)
+    merge = [(ms, w) for run in runs_ for kind, ms, w in run if kind == "mp_merge"]
+    merge_ms = sum(ms for ms, _ in merge) / len(runs_)
+    mcells = sum(w for _, w in merge) / len(runs_)
+    del prep
+    out = {"configs": C, "layers": g.n_layers, "tables": tables, "fold_kernel_ms": fold_ms,
+           "fold_launches": len(fold) // len(runs_), "cell_updates": cells, "plan_ms": plan_ms,
+           "global_cell_updates": global_cells, "ms_by_kernel": by_kind, "cost": r.cost, "precision": r.precision,
+           "k4_merge": {"kernel": "mp_merge_kernel (Eq. 3, int32 add + column minima)", "ms": merge_ms,
+                        "cells": mcells, "bytes": 12.0 * mcells,
+                        "achieved_gbs": 12.0 * mcells / (merge_ms * 1e-3) / 1e9 if merge_ms else None,
+                        "hbm_peak_gbs": peaks().get("hbm_gbs")} if mcells else None}
+    if check and os.path.exists(gold_path) and "reference draw order" in tables:
+        with open(gold_path) as f:
+            gold = json.load(f)
+        out["matches_reference"] = bool([int(x) for x in r.indices] == gold["indices"] and float(r.cost).hex() == gold["cost"])
+        out["reference_cpu_s"] = gold["reference_cpu_s"]
+    elif check:
+        ctx.set_kernel_policy("generic")  # the same device tables through the generic tiled int32 fold
+        try:
+            b = P.plan_with_tables(g, t)
+            out["matches_generic"] = bool(list(b.indices) == list(r.indices) and b.cost == r.cost)
+            out["generic_ms"] = b.device_ms
+        finally:
+            ctx.set_kernel_policy("auto")
+    del t
+    return out
+
+
+def minplus(P, ctx, args, stream, sm_mhz):
+    """Min-plus sweep; the headline roofline is the C=1024 point's mp_fold_kernel."""
+    points = {}
+    for C in args.minplus_sweep:
+        try:
+            points[str(C)] = minplus_point(P, ctx, stream, C, args.minplus_runs, check=not args.no_check)
+        except Exception as exc:  # report, keep the line
+            points[str(C)] = {"error": str(exc)[:300]}
+    f_mhz = sm_mhz or peaks().get("sm_max_mhz", 1965.0)
+    peak_tflops = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # FP32 CUDA-core: 2 ops (add + min) per cell update per lane-clock
+    for pt in points.values():
+        if "fold_kernel_ms" in pt and pt["fold_kernel_ms"]:
+            pt["fold_frac"] = 2.0 * pt["cell_updates"] / (pt["fold_kernel_ms"] * 1e-3) / 1e12 / peak_tflops
+            pt["plan_frac"] = 2.0 * pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3) / 1e12 / peak_tflops
+            pt["plan_cell_updates_per_s"] = pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3)
+    head = points.get(str(args.minplus_c)) or next(iter(points.values()), {})
+    traffic, basis = committed_traffic("mp_fold_kernel")
+    roof = None
+    if head.get("fold_kernel_ms"):
+        achieved = 2.0 * head["cell_updates"] / (head["fold_kernel_ms"] * 1e-3) / 1e12
+        launches = max(1, head["fold_launches"])
+        roof = {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved / peak_tflops, "traffic": traffic, "traffic_basis": basis,
+                "kernel": f"mp_fold_kernel (K3 Eq. 2 fold, VIADDMNMX.U16x2), config-5 graph at C={head['configs']}",
+                "launches": launches, "algorithmic": "2 ops (add + min) per cell update; cells = sum nu*nw*nv",
+                "peak_basis": f"148 SM x 128 FP32 lanes x 2 ops x {f_mhz:.0f} MHz (SM clock sampled under load)",
+                "plan_frac": head.get("plan_frac")}
+    return roof, points
+
+
+def run_ours(args):
+    import numpy as np  # noqa: F401
     import torch
     import torch.distributed as dist
 
@@ -213,7 +456,7 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     ctx = P.Context(local, stream=stream.cuda_stream)
     model, batch, D = workload(args.workload)
-    g = P.builtin_model(model if model != "inception_chain" else "inception_chain", batch)
+    g = P.builtin_model(model, batch)
     dev = P.DeviceGraph.uniform(D)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -246,6 +489,7 @@ def run_ours(args):
     total = torch.tensor([sum(dev_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    # whole-job: N ranks each search their own replica in the max-rank time
     value = total.item() / (args.steps * world)
 
     # ---- e2e: pp_plan through the C ABI with host buffers ------------------------
@@ -280,39 +524,56 @@ def run_ours(args):
 
     # ---- plan_with_tables only (the CLI's planning_ms) ---------------------------------
     t_built = P.build_cost_tables(g, dev, ctx)
-    pwt = P.PreparedPlan(g, tables=t_built, ctx=ctx)
-    pw = []
-    for k in range(args.warmup + args.steps):
-        flush.zero_()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        pwt.launch()
-        s1.record(stream)
-        pwt.fetch()
-        if k >= args.warmup:
-            pw.append(s0.elapsed_time(s1))
+    pw, _ = time_prepared(P, P.PreparedPlan(g, tables=t_built, ctx=ctx), stream, flush, args.steps, args.warmup)
+    gold = golden_builtin(model if model != "inception_chain" else "inception_chain", D)
 
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": max(dev_ms) if world == 1 else value * world, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": value / PAPER_MS, "dtype": "f64",
         "data": "synthetic (builtin model graph, analytic cost tables; each rank searches its own replica)",
-        "config": {"workload": f"plan(inception_chain(12)@{D})" if model == "inception_chain" else args.workload,
-                   "model": model, "batch": batch, "devices": D, "layers": g.n_layers, "edges": g.n_edges,
-                   "l2": "256 MiB write between timed steps", "parallelism": f"replicas x{world}"},
+        "config": config_of(model, batch, D),
+        "config_detail": {"layers": g.n_layers, "edges": g.n_edges, "l2": "256 MiB write between timed steps",
+                          "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "call": "pp_plan(ctx, graph, device_desc, k_bound, host indices) — host prep + H2D + device + D2H"},
+                "call": "pp_plan(ctx, graph, device_desc, k_bound, host indices) on a cached pp_graph: host prep + "
+                        "H2D + device + D2H (see dropin_e2e for parplan::plan() with a fresh graph per call)"},
         "gpu_launches": launches,
         "plan_with_tables_ms": statistics.mean(pw),
         "result": {"cost": r.cost, "node_eliminations": r.node_eliminations, "edge_eliminations": r.edge_eliminations,
-                   "waves": r.waves, "precision": r.precision},
+                   "waves": r.waves, "precision": r.precision,
+                   "matches_reference": bool(gold and [int(x) for x in r.indices] == gold["indices"]
+                                             and float(r.cost).hex() == gold["cost"])},
         "search_kernels": kern,
         "clocks": clk.summary(),
     }
+    if not args.quick:
+        line["models"] = model_sweep(P, ctx, stream, flush, args)
+        if rank == 0:
+            line["dropin_e2e"] = dropin_latency(args)
+        line["k1_table_build"] = table_build(P, ctx)
 
-    # ---- min-plus roofline (config-5 synthetic graph) --------------------------------
-    if args.minplus_c > 0:
-        line.update(minplus(P, ctx, args, flush, stream))
+    # ---- min-plus roofline and sweep (config-5 synthetic graph) ----------------------------
+    if args.minplus_sweep:
+        with Clocks(local) as mclk:
+            roof, points = minplus(P, ctx, args, stream, None)
+        mc = mclk.summary()
+        if mc.get("sm_mhz"):  # re-base the peak on the clock sampled under the min-plus load
+            f = mc["sm_mhz"]
+            pk = 148 * 128 * 2 * f * 1e6 / 1e12
+            for pt in points.values():
+                if pt.get("fold_kernel_ms"):
+                    pt["fold_frac"] = 2.0 * pt["cell_updates"] / (pt["fold_kernel_ms"] * 1e-3) / 1e12 / pk
+                    pt["plan_frac"] = 2.0 * pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3) / 1e12 / pk
+            if roof:
+                roof["peak"] = pk
+                roof["frac"] = roof["achieved"] / pk
+                roof["plan_frac"] = points.get(str(args.minplus_c), {}).get("plan_frac")
+                roof["peak_basis"] = f"148 SM x 128 FP32 lanes x 2 ops x {f:.0f} MHz (SM clock sampled under the min-plus load)"
+        if roof:
+            line["roofline"] = roof
+        line["minplus"] = {"points": points, "clocks": mc,
+                           "workload": "plan_with_tables(series_parallel(seed 1, 1000 layers, bp 0.3), C configs)"}
 
     # ---- CPU baseline: the real reference on the same workload --------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -328,100 +589,18 @@ def run_ours(args):
                                                         f"core; wall time / {procs} (throughput, not the latency)")
         except Exception as exc:
             print(f"parallel reference sample failed: {exc}", file=sys.stderr)
-        line["result"]["matches_reference"] = bool(
+        small = {}
+        for m, d in (("lenet5", 4), ("alexnet", 4)):  # per-call latency where fixed overheads dominate
+            _, ts, _ = reference_plan_ms(m, 32, d, 20, 3)
+            small[f"{m}@{d}"] = statistics.median(ts)
+        line["cpu_baseline"]["small_models_ms"] = small
+        line["result"]["matches_cpu_reference"] = bool(
             list(res_ref.indices) == list(r.indices) and res_ref.cost == r.cost)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def committed_traffic(kernel):
-    """DRAM bytes (read + write) of one launch of `kernel` from the committed
-    ncu --set full summary under profiles/ (the roofline's traffic field)."""
-    import csv
-    import glob
-
-    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_full_summary.csv")),
-                       reverse=True):
-        with open(path) as f:
-            rows = [r for r in csv.DictReader(f) if kernel in r["kernel"]]
-        if not rows:
-            continue
-        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        total = 0.0
-        for r in rows:
-            if r["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                total += float(r["value"]) * scale.get(r["unit"], 1.0)
-        return total, f"{os.path.basename(path)}: dram__bytes_read.sum + dram__bytes_write.sum of one captured launch"
-    return None, "no committed ncu --set full summary"
-
-
-def minplus(P, ctx, args, flush, stream):
-    """Config-5 synthetic sweep point: 1000 layers (bp 0.3, seed 1 topology),
-    C configs per layer, device-generated dyadic tables, exact int32 DP."""
-    import torch
-
-    C = args.minplus_c
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:  # one plan row-sharded across all ranks (NCCL all-gathers at re-association points)
-        from paper_1802_04924_b200 import distributed as PD
-
-        ctx = P.Context(ctx.device, stream=stream.cuda_stream)
-        PD.attach(ctx)
-    g = P.series_parallel_graph(1, 1000, 0.3)
-    t = P.synthetic_cost_tables(g, C, seed=1, ctx=ctx)
-    prep = P.PreparedPlan(g, tables=t, ctx=ctx)
-    prep.launch()
-    r = prep.fetch()
-    global_cells = float(C) ** 3 * sum(1 for rec in g.schedule()[0] if rec[0] == 0)
-    with Clocks(ctx.device) as clk:
-        runs = [prep.profile() for _ in range(args.minplus_runs)]
-    # whole-plan device time of one search, max over ranks
-    starts, ends = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    starts.record(stream)
-    prep.launch()
-    ends.record(stream)
-    prep.fetch()
-    plan_ms = starts.elapsed_time(ends)
-    if world > 1:
-        from paper_1802_04924_b200 import distributed as PD
-
-        plan_ms = PD.max_over_ranks(plan_ms, device="cuda")
-    folds = [(ms, w) for run in runs for kind, ms, w in run if kind == "mp_fold"]
-    if not folds:  # generic path only (no certified large folds)
-        folds = [(ms, w) for run in runs for kind, ms, w in run if kind == "wave"]
-    wave_ms = sum(ms for ms, _ in folds) / len(runs)
-    cells = sum(w for _, w in folds) / len(runs)
-    total_ms = sum(ms for run in runs for _, ms, _ in run) / len(runs)
-    by_kind = {}
-    for run in runs:
-        for kind, ms, _ in run:
-            by_kind[kind] = by_kind.get(kind, 0.0) + ms / len(runs)
-    c = clk.summary()
-    pk = peaks()
-    f_mhz = c["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)
-    sms = 148
-    peak_tflops = sms * 128 * 2 * f_mhz * 1e6 / 1e12  # FP32 CUDA-core: 2 ops (add + min) per cell at 1 cell/lane/clk
-    achieved = 2.0 * cells / (wave_ms * 1e-3) / 1e12
-    traffic, traffic_basis = committed_traffic("mp_fold_kernel")
-    return {
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tflops, "traffic": traffic, "traffic_basis": traffic_basis,
-                     "kernel": "mp_fold_kernel (K3 Eq. 2 fold, VIADDMNMX.S16x2), config-5 graph",
-                     "launches": len(folds) // len(runs),
-                     "peak_basis": f"148 SM x 128 FP32 lanes x 2 ops x {f_mhz:.0f} MHz (measured SM clock under load)"},
-        "minplus": {"configs": C, "layers": g.n_layers, "cell_updates": cells,
-                    "cell_updates_per_s": cells / (wave_ms * 1e-3), "fold_kernel_ms": wave_ms,
-                    "profiled_plan_ms": total_ms, "ms_by_kernel": by_kind,
-                    "plan_ms": plan_ms, "global_cell_updates": global_cells,
-                    "plan_cell_updates_per_s": global_cells / (plan_ms * 1e-3), "ranks": world,
-                    "sharding": "row blocks of c_u across ranks" if world > 1 else "none",
-                    "cost": r.cost, "precision": r.precision, "clocks": c,
-                    "workload": f"plan_with_tables(series_parallel(seed 1, 1000 layers, bp 0.3), C={C})"},
-    }
 
 
 def main():
@@ -431,8 +610,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="inception_chain@16")
-    ap.add_argument("--minplus-c", type=int, default=1024)
+    ap.add_argument("--minplus-c", type=int, default=1024, help="the sweep point the headline roofline is quoted on")
+    ap.add_argument("--minplus-sweep", type=lambda x: [int(c) for c in x.split(",") if c], default=[1024, 2048, 4096])
     ap.add_argument("--minplus-runs", type=int, default=2)
+    ap.add_argument("--no-check", action="store_true", help="skip the min-plus parity checks")
+    ap.add_argument("--quick", action="store_true", help="headline only (no model sweep / drop-in / K1)")
     ap.add_argument("--cpu-runs", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

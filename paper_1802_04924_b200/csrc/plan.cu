@@ -457,6 +457,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     size_t mm0 = 0; // min-plus merges: [mm0, mm0 + nmm) in mmv
     int nmm = 0;
     int64_t mm_blocks = 0;
+    double mm_cells = 0.0;
     std::vector<std::tuple<const void *, void *, size_t>> gathers; // sharded: derived t2 -> full, before the wave
   };
   struct Image {
@@ -783,6 +784,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
               mm.blk_begin = wr.mm_blocks;
               wr.mm_blocks += static_cast<int64_t>((mm.nc + 31) / 32) * ((mm.nr + kMpMergeRows - 1) / kMpMergeRows);
               wr.cells += static_cast<double>(mm.nr) * mm.nc;
+              wr.mm_cells += static_cast<double>(mm.nr) * mm.nc;
               mmv.push_back(mm);
               ++wr.nmm;
               continue;
@@ -1229,7 +1231,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         check_launch(ctx);
       });
       P->step_kind.push_back(9);
-      P->step_work.push_back(0.0);
+      P->step_work.push_back(wr.mm_cells);
       ++launches;
     }
     for (const auto &grp : wr.mg) { // large fixed-point folds of this wave, per launch group: prep -> stream-K fold
