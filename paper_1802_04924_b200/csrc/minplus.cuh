@@ -32,10 +32,11 @@
 // rowspan(a), and likewise <= colspan(b), so cap = M + 1 with
 // M = min(rowspan bound, colspan bound) is always safe (proven); only 2 cap,
 // not spanA + spanB, must fit: (2 cap << JB) + 2^JB - 1 <= 65534.  Static
-// bounds on derived tables are loose, so a fold whose proven JB would be < 5
-// runs optimistically at JB = 5 with the largest JB-5 cap: the epilogue
-// checks m'' < cap for every stored cell and raises `ovf` otherwise, and the
-// host then re-runs the plan with the proven caps.
+// bounds on derived tables are loose and minima of many candidates are small,
+// so folds run optimistically at JB = 6 (64-j groups: half the key updates of
+// JB = 5) with the largest JB-6 cap (511): the epilogue checks m'' < cap for
+// every stored cell and raises `ovf` otherwise, and the host then re-runs the
+// plan with the proven caps (JB <= 5).
 //
 // The group key must order (value, group, j mod 2^JB): per group and cell
 // pair, one LOP3 moves the two j-low fields next to the group id
@@ -128,6 +129,7 @@ inline int mp_jbits(int64_t M) {
     if (((2 * M + 2) << jb) + (1 << jb) - 1 <= 65534) return jb;
   return 0;
 }
+constexpr int kMpOptJB = 6; // optimistic plans: 64-j argmin groups, cap 511 (checked on the device)
 // the largest cap JB bits allow
 inline int32_t mp_max_cap(int jb) { return static_cast<int32_t>((65534 - ((1 << jb) - 1)) >> (jb + 1)); }
 
@@ -487,7 +489,9 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
 
   // consumers: thread (ty, tx) owns rows ty*8..+7, columns tx*8..+7 of the tile
   const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
-  constexpr int G_PER_STAGE = kMpChunk >> JB; // argmin groups per stage
+  // argmin groups of 2^JB j: GPS per stage (JB <= 5) or one per CPG stages (JB = 6)
+  constexpr int GL = (1 << JB) < kMpChunk ? (1 << JB) : kMpChunk; // j of a group inside one stage
+  constexpr int GPS = kMpChunk / GL, CPG = (1 << JB) / GL;
   constexpr uint32_t LOW2 = ((1u << JB) - 1) * 0x10001u;
   int64_t u = u_begin, nn = 0;
   while (u < u_end) {
@@ -499,23 +503,34 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
     const int64_t tile_lo = f.unit_begin + static_cast<int64_t>(tile) * f.nchunks, tile_hi = tile_lo + f.nchunks;
     const int64_t seg_lo = u, seg_end = min(u_end, tile_hi);
 
-    // key = value << (16 + JB) | j (group << JB | j-low): lowest value, then lowest j
-    uint32_t key[8][8];
+    // key = value << (16 + JB) | j (group << JB | j-low): lowest value, then lowest j.
+    // A group cut by a segment boundary contributes its part; parts combine by min.
+    uint32_t key[8][8], m[8][4];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < 8; ++r) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) key[r][q] = 0xFFFFFFFFu;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[r][q] = 0xFFFFFFFFu; // defined on every path (reset at each group start)
+    }
 
     for (int c = c_first; u < seg_end; ++u, ++nn, ++c) {
       const int s = static_cast<int>(nn % kMpStages);
       mbar_wait(&full[s], static_cast<unsigned>(nn / kMpStages) & 1u);
       const uint32_t *As = reinterpret_cast<const uint32_t *>(mp_smem + s * kMpStageBytes) + ty * 8;
       const uint32_t *Bs = reinterpret_cast<const uint32_t *>(mp_smem + s * kMpStageBytes + kMpStageA) + tx * 4;
+      const bool g_start = CPG == 1 || c % CPG == 0 || c == c_first;
+      const bool g_end = CPG == 1 || c % CPG == CPG - 1 || u + 1 == seg_end;
 #pragma unroll
-      for (int g = 0; g < G_PER_STAGE; ++g) {
-        uint32_t m[8][4];
+      for (int g = 0; g < GPS; ++g) {
+        if (g_start) {
 #pragma unroll
-        for (int jj = g << JB; jj < (g + 1) << JB; ++jj) {
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) m[r][q] = 0xFFFFFFFFu; // min(a'' + b'', 0xFFFF) = a'' + b''
+        }
+#pragma unroll
+        for (int jj = g * GL; jj < (g + 1) * GL; ++jj) {
           uint32_t a[8], bb[4];
           *reinterpret_cast<uint4 *>(&a[0]) = *reinterpret_cast<const uint4 *>(As + jj * kMpTile);
           *reinterpret_cast<uint4 *>(&a[4]) = *reinterpret_cast<const uint4 *>(As + jj * kMpTile + 4);
@@ -523,18 +538,19 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
 #pragma unroll
           for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              m[r][q] = jj == (g << JB) ? __vadd2(a[r], bb[q]) : __viaddmin_u16x2(a[r], bb[q], m[r][q]);
+            for (int q = 0; q < 4; ++q) m[r][q] = __viaddmin_u16x2(a[r], bb[q], m[r][q]);
         }
-        const uint32_t G2 = static_cast<uint32_t>(c * G_PER_STAGE + g) * ((1u << JB) * 0x10001u); // group << JB, both halves
+        if (g_end) {
+          const uint32_t G2 = static_cast<uint32_t>((c * kMpChunk + g * GL) >> JB) * ((1u << JB) * 0x10001u); // group << JB, both halves
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+          for (int r = 0; r < 8; ++r)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t gj = (m[r][q] & LOW2) | G2, mv = m[r][q] & ~LOW2;
-            key[r][2 * q] = min(key[r][2 * q], __byte_perm(mv, gj, 0x1054));
-            key[r][2 * q + 1] = min(key[r][2 * q + 1], __byte_perm(mv, gj, 0x3276));
-          }
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t gj = (m[r][q] & LOW2) | G2, mv = m[r][q] & ~LOW2;
+              key[r][2 * q] = min(key[r][2 * q], __byte_perm(mv, gj, 0x1054));
+              key[r][2 * q + 1] = min(key[r][2 * q + 1], __byte_perm(mv, gj, 0x3276));
+            }
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);

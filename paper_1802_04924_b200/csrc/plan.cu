@@ -349,8 +349,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       // every minimum <= min(rowspan(w + t1), colspan(t2)) (minplus.cuh: cap)
       fold_m[oi] = std::min(t.node_span[static_cast<size_t>(op.removed)] + R[a], Kc[b2]);
       fold_jb[oi] = fold_m[oi] < 32768 ? mp_jbits(fold_m[oi]) : 0;
-      // optimistic JB 5 (cap checked in the epilogue) unless conservative
-      if (fold_jb[oi] < 5 && !conservative) fold_opt[oi] = 1, fold_jb[oi] = 5;
+      // optimistic JB 6 (cap 511, checked in the epilogue) unless conservative
+      if (!conservative) fold_opt[oi] = 1, fold_jb[oi] = kMpOptJB;
       large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && fold_jb[oi] > 0 && !ctx->no_minplus;
       if (large[oi] && nu_eff(op.e1) > 0) {
         mp_consumer[a] = static_cast<int>(oi);
@@ -373,7 +373,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     for (int w = 1; w <= s.n_waves; ++w) {
       size_t off = 0, coff = 0;
       int g = 0;
-      wave_group_jb[static_cast<size_t>(w)].assign(1, 5);
+      wave_group_jb[static_cast<size_t>(w)].assign(1, kMpOptJB);
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         if (!large[static_cast<size_t>(oi)]) continue;
@@ -392,7 +392,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           mp_cnt = std::max(mp_cnt, coff);
           off = coff = 0;
           ++g;
-          wave_group_jb[static_cast<size_t>(w)].push_back(5);
+          wave_group_jb[static_cast<size_t>(w)].push_back(kMpOptJB);
         }
         mp_group[static_cast<size_t>(oi)] = g;
         int &gjb = wave_group_jb[static_cast<size_t>(w)].back();
@@ -409,6 +409,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     if (mp_bytes) {
       mp_part = static_cast<size_t>(ctx->sms) * kMpTileCells * 4;
       // per device, every prepare (cheap; no process-wide cache across devices)
+      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
@@ -708,12 +709,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             // original t2: mp_colmin (once per plan); a large fold's or an mp_merge's output: their epilogues
             f.cb_ready = op.e2 < t.ne || (!shard && (mp_producer[static_cast<size_t>(op.e2)] >= 0 ||
                                                      mp_merge_out[static_cast<size_t>(op.e2)]));
-            if (fold_opt[static_cast<size_t>(oi)]) {
-              f.cap = mp_max_cap(f.jb);
-              f.ovf = ovf_ptr();
-            } else {
-              f.cap = static_cast<int32_t>(fold_m[static_cast<size_t>(oi)] + 1);
-            }
             f.nu = nu_eff(op.e1);
             f.nw = t.counts[static_cast<size_t>(op.removed)];
             f.nv = cols[static_cast<size_t>(op.e2)];
@@ -726,6 +721,15 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             if (G.np == 0) G.p0 = mpf.size();
             G.jb = wave_group_jb[static_cast<size_t>(s.ops[static_cast<size_t>(oi)].wave)][static_cast<size_t>(gi)];
             f.jb = G.jb;
+            // operand cap (minplus.cuh): optimistic = the largest the launch's JB allows, checked on
+            // the device; proven = M + 1, which fits the fold's (and so the group's smaller) JB
+            if (fold_opt[static_cast<size_t>(oi)]) {
+              f.cap = mp_max_cap(f.jb);
+              f.ovf = ovf_ptr();
+            } else {
+              f.cap = static_cast<int32_t>(fold_m[static_cast<size_t>(oi)] + 1);
+            }
+            PP_REQUIRE(((2 * int64_t(f.cap)) << f.jb) + (1 << f.jb) - 1 <= 65534, "min-plus operand cap exceeds 16 bits");
             const int batches = (f.nchunks + kMpPrepBatch - 1) / kMpPrepBatch;
             f.a_batches = f.ra_ready ? batches : 1;
             f.b_batches = f.cb_ready ? batches : 1;
@@ -1270,8 +1274,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         cfg.stream = st;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        PP_CUDA(cudaLaunchKernelEx(&cfg, jb == 5 ? mp_fold_kernel<5> : jb == 4 ? mp_fold_kernel<4> : mp_fold_kernel<3>, mf,
-                                   np, units));
+        PP_CUDA(cudaLaunchKernelEx(&cfg,
+                                   jb == 6   ? mp_fold_kernel<6>
+                                   : jb == 5 ? mp_fold_kernel<5>
+                                   : jb == 4 ? mp_fold_kernel<4>
+                                             : mp_fold_kernel<3>,
+                                   mf, np, units));
         check_launch(ctx);
       });
       P->step_kind.push_back(8);

@@ -46,13 +46,13 @@ def short(name: str) -> str:
     return name.split("<")[0] if not name.startswith("at::") else name
 
 
-def launches(tag: str) -> None:
-    src = os.path.join(OUT, "launches.csv")
+def launches(tag: str, src_name: str = "launches.csv", out_name: str = "bench_launches") -> None:
+    src = os.path.join(OUT, src_name)
     lines = [l for l in open(src) if l.startswith('"')]
     rows = list(csv.DictReader(io.StringIO("".join(lines))))
     raw = [(r["Kernel Name"], float(r["Metric Value"]) / 1000.0) for r in rows
            if r["Metric Name"] == "gpu__time_duration.sum"]
-    with open(os.path.join(PROF, f"{tag}_bench_launches_raw.csv"), "w", newline="") as f:
+    with open(os.path.join(PROF, f"{tag}_{out_name}_raw.csv"), "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "us"])
         for k, us in raw:
@@ -61,7 +61,7 @@ def launches(tag: str) -> None:
     for k, us in raw:
         agg["pp::" + short(k) if "pp::" in k else short(k)].append(us)
     total = sum(us for _, us in raw)
-    with open(os.path.join(PROF, f"{tag}_bench_launches_summary.csv"), "w", newline="") as f:
+    with open(os.path.join(PROF, f"{tag}_{out_name}_summary.csv"), "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "launches", "total_us", "mean_us", "share_of_profiled_time"])
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
@@ -88,6 +88,8 @@ def main() -> int:
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     shutil.copy(os.path.join(OUT, "bench_plain.json"), os.path.join(PROF, f"{tag}_bench_line.json"))
     launches(tag)
+    if os.path.exists(os.path.join(OUT, "launches_mp1024.csv")):
+        launches(tag, "launches_mp1024.csv", "minplus_c1024_launches")
     for name in sys.argv[2:] or ["mp_fold_full", "fused_full"]:
         ncu_summary(tag, name)
     return 0
