@@ -160,6 +160,19 @@ pp_status pp_context_set_kernel_policy(pp_context *ctx, int32_t policy);
  * NCCL is loaded at run time (libnccl.so.2); no link-time dependency. */
 pp_status pp_comm_unique_id(void *id128);
 pp_status pp_context_attach_comm(pp_context *ctx, int32_t nranks, int32_t rank, const void *id128);
+/* Virtual ranks: n contexts on ONE device run a row-sharded plan through the
+ * multi-GPU code path (row blocks of c_u, all-gathers of derived t2 at
+ * re-association points and of the final edges, the distributed unwind that
+ * reads each record's argmin row from its owner rank), each all-gather being
+ * one device-to-device copy per rank block.  Results equal the single-GPU
+ * plan bit for bit.  pp_vgroup_plan: give exactly one of dev (build_cost_tables
+ * + plan on every rank, planner.hpp:368-371) and t (plan_with_tables,
+ * planner.hpp:339-364; the tables are shared by the ranks). */
+typedef struct pp_vgroup pp_vgroup;
+pp_status pp_vgroup_create(int32_t device, int32_t nranks, pp_vgroup **out);
+pp_status pp_vgroup_plan(pp_vgroup *group, const pp_graph *g, const pp_device_desc *dev, pp_tables *t,
+                         int32_t k_bound, int32_t *indices, pp_plan_result *res);
+pp_status pp_vgroup_destroy(pp_vgroup *group);
 /* kernel launches issued on this context since creation */
 pp_status pp_context_launch_count(const pp_context *ctx, int64_t *launches);
 

@@ -16,6 +16,7 @@ from .capi import (  # noqa: F401
     ParplanError,
     PlanResult,
     PreparedPlan,
+    VirtualRanks,
     ReducedGraph,
     brute_force_plan,
     build_cost_tables,

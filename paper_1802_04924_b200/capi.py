@@ -15,6 +15,7 @@ raises, and every table/plan call needs an sm_100 GPU.
 from __future__ import annotations
 
 import ctypes as C
+import time
 import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -89,6 +90,9 @@ _SIGS = {
     "pp_comm_unique_id": (C.c_int, [C.c_char_p]),
     "pp_context_attach_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_char_p]),
     "pp_context_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "pp_vgroup_create": (C.c_int, [C.c_int32, C.c_int32, _pp]),
+    "pp_vgroup_plan": (C.c_int, [_vp, _vp, C.c_void_p, _vp, C.c_int32, _i32p, C.POINTER(_PlanResult)]),
+    "pp_vgroup_destroy": (C.c_int, [_vp]),
     "pp_graph_create": (C.c_int, [C.POINTER(_GraphDesc), _pp]),
     "pp_graph_builtin": (C.c_int, [C.c_char_p, C.c_int64, _pp]),
     "pp_graph_destroy": (C.c_int, [_vp]),
@@ -555,6 +559,34 @@ def plan(graph: ComputationGraph, devices: DeviceGraph, k_bound: int = 8, ctx: O
     d = devices._desc()
     _check(lib().pp_plan(ctx.h, graph.h, C.byref(d), k_bound, idx, C.byref(r)))
     return _result(idx, r)
+
+
+class VirtualRanks:
+    """pp_vgroup: n contexts on one device run the row-sharded (multi-GPU) plan
+    path; all-gathers are device-to-device copies, the unwind reads argmin rows
+    from their owner rank.  Results equal the single-GPU plan bit for bit."""
+
+    def __init__(self, nranks: int, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().pp_vgroup_create(device, nranks, C.byref(h)))
+        self.h, self.nranks = h, nranks
+
+    def plan(self, graph: ComputationGraph, devices: Optional[DeviceGraph] = None,
+             tables: Optional[CostTables] = None, k_bound: int = 8) -> PlanResult:
+        idx = np.zeros(graph.n_layers, np.int32)
+        r = _PlanResult()
+        d = devices._desc() if devices is not None else None
+        t0 = time.perf_counter()
+        _check(lib().pp_vgroup_plan(self.h, graph.h, C.cast(C.pointer(d), C.c_void_p) if d is not None else None,
+                                    tables.h if tables is not None else None, k_bound, idx, C.byref(r)))
+        out = _result(idx, r)
+        out.wall_ms = (time.perf_counter() - t0) * 1e3
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().pp_vgroup_destroy(self.h)
+            self.h = None
 
 
 class PreparedPlan:

@@ -830,7 +830,8 @@ struct UnwindRec {
   const uint16_t *am; // argmins [rows][cols]; a chain record: path table [rows][cols][n]
   int32_t removed, src, dst, cols;
   int32_t n;          // 0: one fold; n > 0: a chain of n folds whose removed nodes are chain_nodes[removed, removed + n)
-  int32_t pad;
+  int32_t blk;        // row-sharded plan: rows per rank; `am` is then the table's byte offset in every
+                      // rank's plan memory and row r is read from rank r / blk (FinishArgs::peer)
 };
 
 struct FinishArgs {
@@ -863,6 +864,7 @@ struct FinishArgs {
   int ne;
   double *cost;
   uint64_t *trace; // optional: stamps after each finish step (profiling)
+  const unsigned char *const *peer; // row-sharded: plan memory base of every rank (peer / IPC mapped)
   int32_t smem_ok;  // the caller's shared memory holds indices[nl] + terms[nl + ne]
 };
 
@@ -973,7 +975,11 @@ template <class T> __device__ __forceinline__ void finish_block(const FinishArgs
     for (int q = a.group_begin[gidx] + threadIdx.x; q < a.group_begin[gidx + 1]; q += kFinishThreads) {
       const UnwindRec r = q == a.group_begin[gidx] + static_cast<int>(threadIdx.x) && have ? u : a.recs[q];
       const int64_t at = static_cast<int64_t>(idx[r.src]) * r.cols + idx[r.dst];
-      if (r.n == 0) {
+      if (r.blk > 0) { // distributed unwind: the owner rank's argmin row, read over NVLink / peer memory
+        const int row = idx[r.src], q = row / r.blk;
+        const uint16_t *am = reinterpret_cast<const uint16_t *>(a.peer[q] + reinterpret_cast<uintptr_t>(r.am));
+        idx[r.removed] = am[static_cast<int64_t>(row - q * r.blk) * r.cols + idx[r.dst]];
+      } else if (r.n == 0) {
         idx[r.removed] = r.am[at];
       } else {
         // the path in batches: all loads of a batch in flight before its

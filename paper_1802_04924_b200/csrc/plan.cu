@@ -111,6 +111,12 @@ struct pp_prepared {
   size_t image_off = 0, image_bytes = 0, res_off = 0, res_bytes = 0, off_idx = 0, off_cost = 0, off_ovf = 0;
   bool mp_conservative = false; // min-plus folds with proven caps only (after an optimistic overflow)
   int k_bound = 8;
+  // row-sharded plans: image offset of the peer bases, rank count, the
+  // all-gather lists of the kind-15 steps (in order), IPC-opened peer bases
+  size_t off_peer = SIZE_MAX;
+  int nranks = 1;
+  std::vector<std::vector<std::tuple<const void *, void *, size_t>>> gather_lists;
+  std::vector<void *> ipc_opened;
   std::vector<std::function<void(cudaStream_t)>> steps;
   int launches_per_run = 0;
   cudaGraph_t graph = nullptr;
@@ -130,6 +136,7 @@ struct pp_prepared {
   ~pp_prepared() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    for (void *p : ipc_opened) cudaIpcCloseMemHandle(p);
   }
 };
 
@@ -244,7 +251,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // is all-gathered first (the re-association points); at the end the final
   // edges and every argmin table are all-gathered so every rank enumerates and
   // unwinds identically.
-  const int NR = ctx->comm ? ctx->nranks : 1, RK = ctx->comm ? ctx->rank : 0;
+  const int NR = ctx->nranks > 1 ? ctx->nranks : 1, RK = NR > 1 ? ctx->rank : 0;
   const bool shard = NR > 1;
   auto blk = [&](int id) { return (rows[static_cast<size_t>(id)] + NR - 1) / NR; };
   auto lr0 = [&](int id) { return std::min(rows[static_cast<size_t>(id)], RK * blk(id)); };
@@ -265,8 +272,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   const bool keep_all = derived_total <= (size_t(4) << 30);
   OffsetPlanner tab_plan;
   std::vector<size_t> tab_off(static_cast<size_t>(E_total), 0), am_off(s.ops.size(), 0);
-  std::vector<size_t> amfull_off(s.ops.size(), 0), gat_off(static_cast<size_t>(E_total), SIZE_MAX);
-  size_t am_bytes = 0, amfull_bytes = 0, gat_bytes = 0;
+  std::vector<size_t> gat_off(static_cast<size_t>(E_total), SIZE_MAX);
+  size_t am_bytes = 0, gat_bytes = 0;
   std::vector<int> prod_wave(static_cast<size_t>(E_total), 0); // wave writing each table (0: original)
   for (int w = 1; w <= s.n_waves; ++w) {
     const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
@@ -279,8 +286,6 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         am_off[static_cast<size_t>(oi)] = am_bytes;
         am_bytes += align256(store_cells(op.ne) * 2);
         if (shard) {
-          amfull_off[static_cast<size_t>(oi)] = amfull_bytes;
-          amfull_bytes += align256(full_cells(op.ne) * 2);
           if (op.e2 >= t.ne) { // derived t2: gathered in full before the fold
             gat_off[static_cast<size_t>(op.e2)] = gat_bytes;
             gat_bytes += align256(full_cells(op.e2) * sizeof(T));
@@ -421,8 +426,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
   const size_t off_tables = 0, off_derived = tables_bytes, off_am = off_derived + align256(tab_plan.end()),
                off_mp = off_am + align256(am_bytes), off_mpp = off_mp + align256(mp_bytes),
-               off_amfull = off_mpp + align256(mp_pbytes),
-               off_gat = off_amfull + align256(amfull_bytes), off_image = off_gat + align256(gat_bytes);
+               off_gat = off_mpp + align256(mp_pbytes), off_image = off_gat + align256(gat_bytes);
 
   // ---- enumeration / unwind descriptors (pointer-free parts) ----------------
   std::vector<int> pos(static_cast<size_t>(t.nl), -1);
@@ -468,6 +472,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     size_t oF, oM, oN, oE, oR, oL, oCO, oXO, oS, oD, oC, oBV, oBI, oRes, oIdx, oFC, oLay, oEdg, oCfg, oRat, oBw, oMP;
     size_t oG, oT, oFW, oST, oTR, oCN; // oT, oST, oTR (+1), oBV, oBI: scratch offsets
     size_t oOvf = 0;                   // min-plus optimistic-cap overflow flag (result slot)
+    size_t oPeer = 0;                  // row-sharded: NR plan memory bases
     size_t scratch = 0;                // bytes of the scratch section
     int n_phases = 0;                // fused kernel: waves / chain segments
     size_t dyn_smem = 0;             // fused kernel dynamic shared memory
@@ -603,6 +608,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     im.oIdx = im.oRes;
     im.oFC = im.pk.put(std::vector<double>(2));
     im.oOvf = im.pk.put(std::vector<int32_t>(4));
+    // row-sharded: every rank's plan memory base (filled before upload: IPC-mapped peers, or the virtual ranks')
+    im.oPeer = shard ? im.pk.put(std::vector<uint64_t>(static_cast<size_t>(NR))) : 0;
     im.res_bytes = im.oOvf + 16 - im.oRes;
     auto ovf_ptr = [&] { return reinterpret_cast<uint32_t *>(db + off_image + im.oOvf); };
     auto scr = [&](size_t bytes) {
@@ -969,15 +976,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       ee.push_back(EnumEdge{t2p(id), pos[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])],
                             pos[static_cast<size_t>(s.edst[static_cast<size_t>(id)])], cols[static_cast<size_t>(id)], 0});
     }
-    auto amfullp = [&](int oi) {
-      return shard ? reinterpret_cast<uint16_t *>(db + off_amfull + amfull_off[static_cast<size_t>(oi)]) : amp(oi);
-    };
-    if (shard)
-      for (size_t oi = 0; oi < s.ops.size(); ++oi)
-        if (!s.ops[oi].type)
-          im.final_gathers.emplace_back(amp(static_cast<int>(oi)), amfullp(static_cast<int>(oi)),
-                                        static_cast<size_t>(blk(s.ops[oi].ne)) *
-                                            cols[static_cast<size_t>(s.ops[oi].ne)] * 2);
+    // row-sharded: argmin tables stay on their ranks; the unwind reads the
+    // owner's row through the peer bases (no gather of the argmin tables)
     // unwind records (kernels.cuh finish_block), visited last wave first and
     // grouped by dependency level: a record's endpoints are final nodes
     // (level 0) or removed by records of lower levels, so one group per
@@ -998,7 +998,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
           PP_REQUIRE(lu >= 0 && lv >= 0, "unwind: record endpoint not yet assigned");
           const int level = std::max(lu, lv) + 1;
           if (ch < 0) {
-            recs.push_back(UnwindRec{amfullp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)], 0, 0});
+            if (shard) // byte offset of the table in every rank's plan memory (identical layouts)
+              recs.push_back(UnwindRec{reinterpret_cast<const uint16_t *>(off_am + am_off[static_cast<size_t>(oi)]),
+                                       op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)], 0, blk(op.ne)});
+            else
+              recs.push_back(UnwindRec{amp(oi), op.removed, op.u, op.v, cols[static_cast<size_t>(op.ne)], 0, 0});
             lvl[static_cast<size_t>(op.removed)] = level;
           } else {
             const ChainRec &cr = chain_recs[static_cast<size_t>(ch)];
@@ -1147,6 +1151,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->off_idx = im.oIdx;
   P->off_cost = im.oFC;
   P->off_ovf = im.oOvf;
+  P->off_peer = shard ? im.oPeer : SIZE_MAX;
+  P->nranks = NR;
 
   if (bp) { // tables live in the plan's memory
     t.node.view(db + off_tables, static_cast<size_t>(t.ncells));
@@ -1159,6 +1165,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->steps.clear();
   P->step_kind.clear();
   P->step_work.clear();
+  P->gather_lists.clear();
   int launches = 0;
   // one cooperative kernel for the whole plan when no fold needs the S16x2 path
   // (use_fused / fused_nc are decided before the image is built)
@@ -1169,10 +1176,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       double bytes = 0.0;
       for (const auto &x : part) bytes += static_cast<double>(std::get<2>(x)) * NR;
       P->steps.push_back([ctx, part](cudaStream_t st) {
+        PP_REQUIRE(ctx->comm, "row-sharded plan without a communicator (virtual ranks run through pp_vgroup)");
         group_start();
         for (const auto &x : part) all_gather(ctx, std::get<0>(x), std::get<1>(x), std::get<2>(x), st);
         group_end();
       });
+      P->gather_lists.push_back(part); // the k-th kind-15 step (virtual ranks copy these blocks themselves)
       P->step_kind.push_back(15);
       P->step_work.push_back(bytes);
     }
@@ -1329,6 +1338,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     fa.digits = fa.indices + t.nl;
     fa.final_cost = reinterpret_cast<double *>(dimg + im.oFC);
     fa.cost = fa.final_cost + 1;
+    fa.peer = shard ? reinterpret_cast<const unsigned char *const *>(dimg + im.oPeer) : nullptr;
     fa.shift = t.shift;
     fa.recs = reinterpret_cast<const UnwindRec *>(dimg + im.oR);
     fa.chain_nodes = reinterpret_cast<const int32_t *>(dimg + im.oCN);
@@ -1461,6 +1471,40 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   P->launches_per_run = launches + (early ? 1 : 0);
 }
 
+// Row-sharded plans over NCCL: every rank's plan memory base, mapped into this
+// process with CUDA IPC (peer memory over NVLink), so the finish phase reads
+// each unwind record's argmin row from the rank that owns it instead of
+// all-gathering every argmin table (planner.hpp:309-319 needs one entry per
+// record).  Plan memory layouts are identical on all ranks up to the argmin
+// tables (row blocks are padded to blk rows), so one offset serves every rank.
+static void exchange_peers(pp_prepared *P) {
+  pp_context *ctx = P->ctx;
+  const int NR = P->nranks;
+  PP_REQUIRE(!P->transient && P->dmem.p, "row-sharded plans own their memory");
+  cudaIpcMemHandle_t mine;
+  PP_CUDA(cudaIpcGetMemHandle(&mine, P->dmem.p));
+  DBuf<unsigned char> buf(sizeof(mine) * static_cast<size_t>(NR));
+  unsigned char *slot = buf.p + sizeof(mine) * static_cast<size_t>(ctx->rank);
+  PP_CUDA(cudaMemcpyAsync(slot, &mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+  all_gather(ctx, slot, buf.p, sizeof(mine), ctx->stream); // in place
+  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(NR));
+  PP_CUDA(cudaMemcpyAsync(all.data(), buf.p, buf.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+  PP_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<uint64_t> bases(static_cast<size_t>(NR));
+  for (int q = 0; q < NR; ++q) {
+    if (q == ctx->rank) {
+      bases[static_cast<size_t>(q)] = reinterpret_cast<uint64_t>(P->dmem.p);
+      continue;
+    }
+    void *p = nullptr;
+    PP_CUDA(cudaIpcOpenMemHandle(&p, all[static_cast<size_t>(q)], cudaIpcMemLazyEnablePeerAccess));
+    P->ipc_opened.push_back(p);
+    bases[static_cast<size_t>(q)] = reinterpret_cast<uint64_t>(p);
+  }
+  std::memcpy(P->hbase + P->off_peer, bases.data(), bases.size() * 8);
+  P->uploaded = false;
+}
+
 static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
   P->k_bound = k_bound;
   BuildPlan bp;
@@ -1479,6 +1523,7 @@ static void prepare(pp_prepared *P, const pp_device_desc *dev, int k_bound) {
     build_steps<double>(P, dev ? &bp : nullptr, k_bound);
   else
     build_steps<int32_t>(P, dev ? &bp : nullptr, k_bound);
+  if (P->nranks > 1 && P->ctx->comm) exchange_peers(P);
 }
 
 // captures the plan's device work as one CUDA graph, on a private stream
@@ -1582,7 +1627,7 @@ void run_plan(pp_context *ctx, Graph &g, Tables *t, const pp_device_desc *dev, i
   P.ctx = ctx;
   P.g = &g;
   P.t = t;
-  P.transient = true;
+  P.transient = ctx->nranks <= 1; // row-sharded plans own their memory (peer-mapped for the unwind)
   PP_CUDA(cudaSetDevice(ctx->device));
   prepare(&P, dev, k_bound);
   const auto t1 = std::chrono::steady_clock::now();
@@ -1775,6 +1820,130 @@ pp_status pp_plan_profile(pp_prepared *P, int32_t cap, double *step_ms, int32_t 
       if (step_work) step_work[k] = work_v[k];
     }
     for (auto &e : ev) cudaEventDestroy(e);
+  });
+}
+
+// ---- virtual ranks: the row-sharded plan on one device ----------------------
+// n contexts on one GPU play the n ranks of a row-sharded plan (the multi-GPU
+// code path: row blocks, all-gathers of derived t2 at re-association points and
+// of the final edges, the distributed unwind through peer bases).  One host
+// thread drives the ranks' step lists in lock-step; an all-gather is one
+// device-to-device copy per (rank, block) after every rank's preceding steps.
+struct pp_vgroup {
+  int device = 0, n = 0;
+  std::vector<pp_context *> ctx;
+  ~pp_vgroup() {
+    for (pp_context *c : ctx) pp_context_destroy(c);
+  }
+};
+
+namespace pp {
+static void run_group(std::vector<pp_prepared *> &Ps) {
+  const int n = static_cast<int>(Ps.size());
+  std::vector<uint64_t> bases(static_cast<size_t>(n));
+  for (int r = 0; r < n; ++r) bases[static_cast<size_t>(r)] = reinterpret_cast<uint64_t>(Ps[static_cast<size_t>(r)]->dmem.p);
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(n));
+  for (auto &e : ev) PP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (int r = 0; r < n; ++r) {
+    pp_prepared &P = *Ps[static_cast<size_t>(r)];
+    std::memcpy(P.hbase + P.off_peer, bases.data(), bases.size() * 8);
+    P.ctx->begin();
+    PP_CUDA(cudaMemcpyAsync(P.dbase + P.image_off, P.hbase, P.image_bytes, cudaMemcpyHostToDevice, P.ctx->stream));
+    P.uploaded = true;
+  }
+  std::vector<size_t> pos(static_cast<size_t>(n), 0);
+  for (size_t k = 0;; ++k) {
+    int at_gather = 0;
+    for (int r = 0; r < n; ++r) {
+      pp_prepared &P = *Ps[static_cast<size_t>(r)];
+      size_t &i = pos[static_cast<size_t>(r)];
+      while (i < P.steps.size() && P.step_kind[i] != 15) P.steps[i++](P.ctx->stream);
+      PP_CUDA(cudaEventRecord(ev[static_cast<size_t>(r)], P.ctx->stream));
+      at_gather += i < P.steps.size();
+    }
+    if (at_gather == 0) break;
+    PP_REQUIRE(at_gather == n, "virtual ranks disagree on the all-gather schedule");
+    for (int r = 0; r < n; ++r) {
+      pp_prepared &P = *Ps[static_cast<size_t>(r)];
+      for (int q = 0; q < n; ++q)
+        if (q != r) PP_CUDA(cudaStreamWaitEvent(P.ctx->stream, ev[static_cast<size_t>(q)], 0));
+      const auto &mine = P.gather_lists[k];
+      for (size_t j = 0; j < mine.size(); ++j) {
+        const size_t bytes = std::get<2>(mine[j]);
+        unsigned char *recv = static_cast<unsigned char *>(std::get<1>(mine[j]));
+        for (int q = 0; q < n; ++q) {
+          const auto &theirs = Ps[static_cast<size_t>(q)]->gather_lists[k];
+          PP_REQUIRE(theirs.size() == mine.size() && std::get<2>(theirs[j]) == bytes, "all-gather blocks differ");
+          PP_CUDA(cudaMemcpyAsync(recv + static_cast<size_t>(q) * bytes, std::get<0>(theirs[j]), bytes,
+                                  cudaMemcpyDeviceToDevice, P.ctx->stream));
+        }
+      }
+      ++pos[static_cast<size_t>(r)];
+    }
+    // the sends of this gather are read by every rank's copies: a rank may not
+    // overwrite them (later waves) before those copies ran
+    for (int r = 0; r < n; ++r) PP_CUDA(cudaEventRecord(ev[static_cast<size_t>(r)], Ps[static_cast<size_t>(r)]->ctx->stream));
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q)
+        if (q != r) PP_CUDA(cudaStreamWaitEvent(Ps[static_cast<size_t>(r)]->ctx->stream, ev[static_cast<size_t>(q)], 0));
+  }
+  // the finish phase of each rank reads the other ranks' argmin tables
+  for (int r = 0; r < n; ++r) {
+    pp_prepared &P = *Ps[static_cast<size_t>(r)];
+    PP_CUDA(cudaEventRecord(P.ctx->ev1, P.ctx->stream));
+    P.launched = true;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+}
+} // namespace pp
+
+pp_status pp_vgroup_create(int32_t device, int32_t nranks, pp_vgroup **out) {
+  return guard([&] {
+    PP_REQUIRE(out && nranks >= 1 && nranks <= 64, "pp_vgroup_create: 1..64 ranks");
+    auto g = std::make_unique<pp_vgroup>();
+    g->device = device;
+    g->n = nranks;
+    for (int r = 0; r < nranks; ++r) {
+      pp_context *c = nullptr;
+      const pp_status st = pp_context_create(device, &c);
+      if (st != PP_OK) fail(st, pp_last_error());
+      c->nranks = nranks;
+      c->rank = r;
+      g->ctx.push_back(c);
+    }
+    *out = g.release();
+  });
+}
+
+pp_status pp_vgroup_destroy(pp_vgroup *g) {
+  delete g;
+  return PP_OK;
+}
+
+pp_status pp_vgroup_plan(pp_vgroup *grp, const pp_graph *g, const pp_device_desc *dev, pp_tables *t, int32_t k_bound,
+                         int32_t *indices, pp_plan_result *res) {
+  return guard([&] {
+    PP_REQUIRE(grp && g && indices && (dev != nullptr) != (t != nullptr), "pp_vgroup_plan: give exactly one of dev, t");
+    std::vector<std::unique_ptr<pp_prepared>> own;
+    std::vector<pp_prepared *> Ps;
+    for (pp_context *c : grp->ctx) {
+      auto P = std::make_unique<pp_prepared>();
+      P->ctx = c;
+      P->g = &const_cast<pp_graph *>(g)->impl;
+      P->t = t ? &t->impl : nullptr;
+      P->transient = false;
+      PP_CUDA(cudaSetDevice(c->device));
+      prepare(P.get(), dev, k_bound);
+      Ps.push_back(P.get());
+      own.push_back(std::move(P));
+    }
+    run_group(Ps);
+    fetch(Ps[0], indices, res);
+    for (size_t r = 1; r < Ps.size(); ++r) { // every rank unwinds the same plan
+      std::vector<int32_t> mine(static_cast<size_t>(g->impl.nl));
+      fetch(Ps[r], mine.data(), nullptr);
+      PP_REQUIRE(std::equal(mine.begin(), mine.end(), indices), "virtual ranks returned different plans");
+    }
   });
 }
 

@@ -72,3 +72,53 @@ def test_row_sharded_plans_match_single_gpu():
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert p.stdout.count(": OK") == n
+
+
+# ---- virtual ranks: the row-sharded plan path on one B200 ------------------------
+
+GOLD = None
+
+
+def _gold():
+    global GOLD
+    if GOLD is None:
+        import json
+
+        GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_golden.json")))
+    return GOLD
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("case", [("inception_chain", 16), ("inception_chain", 64), ("vgg16", 16),
+                                  ("inception_chain(3)", 4), ("alexnet", 4)], ids=lambda c: f"{c[0]}@{c[1]}")
+def test_virtual_ranks_builtin_match_reference(gpu, n, case):
+    """n virtual ranks (row blocks, K1/K2 on every rank, all-gathers at the
+    re-association points, distributed unwind) vs the reference golden."""
+    import paper_1802_04924_b200 as P
+
+    model, D = case
+    gold = next(c for c in _gold()["builtins"] if c["model"] == model and c["devices"] == D)
+    vr = P.VirtualRanks(n)
+    r = vr.plan(P.builtin_model(model, 32), devices=P.DeviceGraph.uniform(D))
+    assert [int(x) for x in r.indices] == gold["indices"]
+    assert float(r.cost).hex() == gold["cost"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("C", [256, 700])
+def test_virtual_ranks_config5_match_single_gpu(gpu, n, C):
+    """Config-5 graph (U16 min-plus folds, row-sharded with proven caps): the
+    same indices and cost as one GPU; at C = 256 also the real reference."""
+    import json
+
+    import paper_1802_04924_b200 as P
+
+    g, t = P.synthetic_instance(1, 1000 if C == 256 else 300, C, 0.3, ctx=gpu.ctx)
+    one = P.plan_with_tables(g, t)
+    r = P.VirtualRanks(n).plan(g, tables=t)
+    assert list(r.indices) == list(one.indices) and r.cost == one.cost
+    if C == 256:
+        gold = next(c for c in _gold()["synthetic"] if c["configs"] == 256)
+        assert [int(x) for x in r.indices] == gold["indices"] and float(r.cost).hex() == gold["cost"]
