@@ -439,6 +439,62 @@ def minplus(P, ctx, args, stream, sm_mhz):
     return roof, points
 
 
+def sharded(P, args, local, stream, flush):
+    """One plan row-sharded across all ranks (pp_context_attach_comm: rows of
+    c_u in blocks, NCCL all-gathers of derived t2 at re-association points and
+    of the final edges, the unwind reading argmin rows from their owner rank
+    through CUDA IPC).  Device ms = max over ranks (strong scaling: the total
+    work is fixed as N grows)."""
+    import torch
+
+    from paper_1802_04924_b200 import distributed as PD
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sctx = P.Context(local, stream=stream.cuda_stream)
+    PD.attach(sctx)
+    out = {"ranks": world}
+    # Inception-v3 stand-in on 64 virtual devices (BASELINE config 4)
+    g = P.builtin_model("inception_chain", 32)
+    prep = P.PreparedPlan(g, devices=P.DeviceGraph.uniform(64), ctx=sctx)
+    ms, r = time_prepared(P, prep, stream, flush, args.steps, args.warmup)
+    gold = golden_builtin("inception_chain", 64)
+    out["inception_chain@64"] = {
+        "device_ms": PD.max_over_ranks(statistics.mean(ms), device="cuda"),
+        "matches_reference": bool(gold and [int(x) for x in r.indices] == gold["indices"]
+                                  and float(r.cost).hex() == gold["cost"]),
+        "note": "K1/K2 on every rank, row-sharded DP; latency-bound, sharding is not expected to help (SURVEY §8e)"}
+    del prep
+    # the min-plus config-5 graph at C = shard_c
+    C = args.shard_c
+    g = P.series_parallel_graph(1, 1000, 0.3)
+    t = P.synthetic_cost_tables(g, C, seed=1, ctx=sctx)
+    prep = P.PreparedPlan(g, tables=t, ctx=sctx)
+    prep.launch()
+    r = prep.fetch()
+    best = 1e30
+    for _ in range(2):
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        prep.launch()
+        s1.record(stream)
+        prep.fetch()
+        best = min(best, s0.elapsed_time(s1))
+    plan_ms = PD.max_over_ranks(best, device="cuda")
+    folds = sum(1 for rec in g.schedule()[0] if rec[0] == 0)
+    cells = float(C) ** 3 * folds
+    prof = prep.profile()
+    ag = sum(ms for k, ms, _ in prof if k == "allgather")
+    agb = sum(w for k, _, w in prof if k == "allgather")
+    peak = 148 * 128 * 2 * 1965e6 * world / 1e12
+    out[f"minplus_C{C}"] = {"plan_ms": plan_ms, "cell_updates": cells, "cell_updates_per_s": cells / (plan_ms * 1e-3),
+                            "plan_frac_of_n_gpus": 2.0 * cells / (plan_ms * 1e-3) / 1e12 / peak,
+                            "allgather_ms_profiled": ag, "allgather_bytes": agb, "cost": r.cost,
+                            "sharding": "row blocks of c_u; derived t2 all-gathered before its fold"}
+    del prep, t
+    return out
+
+
 def run_ours(args):
     import numpy as np  # noqa: F401
     import torch
@@ -575,6 +631,13 @@ def run_ours(args):
         line["minplus"] = {"points": points, "clocks": mc,
                            "workload": "plan_with_tables(series_parallel(seed 1, 1000 layers, bp 0.3), C configs)"}
 
+    # ---- N > 1: the row-sharded plans (one plan across all ranks, NCCL) -----------------
+    if world > 1 and not args.no_shard:
+        try:
+            line["sharded"] = sharded(P, args, local, stream, flush)
+        except Exception as exc:  # report, keep the line
+            line["sharded"] = {"error": str(exc)[:300]}
+
     # ---- CPU baseline: the real reference on the same workload --------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
         kind, times, res_ref = reference_plan_ms(model, batch, D, args.cpu_runs)
@@ -615,6 +678,8 @@ def main():
     ap.add_argument("--minplus-runs", type=int, default=2)
     ap.add_argument("--no-check", action="store_true", help="skip the min-plus parity checks")
     ap.add_argument("--quick", action="store_true", help="headline only (no model sweep / drop-in / K1)")
+    ap.add_argument("--shard-c", type=int, default=4096, help="N > 1: configs of the row-sharded min-plus plan")
+    ap.add_argument("--no-shard", action="store_true", help="N > 1: skip the row-sharded plans")
     ap.add_argument("--cpu-runs", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
