@@ -378,7 +378,7 @@ def minplus_point(P, ctx, stream, C, runs, check):
     for run in runs_:
         for kind, ms, _ in run:
             by_kind[kind] = by_kind.get(kind, 0.0) + ms / len(runs_)
-    fold = [(ms, w) for run in runs_ for kind, ms, w in run if kind == "mp_fold"]
+    fold = [(ms, w) for run in runs_ for kind, ms, w in run if kind in ("mp_fold", "mp_chain")]
     fold_ms = sum(ms for ms, _ in fold) / len(runs_)
     cells = sum(w for _, w in fold) / len(runs_)
     merge = [(ms, w) for run in runs_ for kind, ms, w in run if kind == "mp_merge"]

@@ -106,7 +106,8 @@ struct MpFold {
   int32_t cap;   // operand cap: M + 1 (proven), or the JB's largest when optimistic
   uint32_t *ovf; // optimistic cap: set when a minimum reaches the cap (the host re-plans conservatively)
   int32_t ra_ready, cb_ready; // minima supplied before mp_prep (epilogue / mp_colmin)
-  int32_t a_batches, b_batches; // mp_prep blocks per row group / column group (chunk batches)
+  int32_t a_batches, b_batches; // mp_prep blocks per row group / column group (chunk batches; 0: none)
+  int32_t b_cols;               // B row width: 0 = 128-column tiles (mp_fold); kMpChainCols (mp_chain)
   int64_t prep_begin;   // first mp_prep block (A blocks, then B blocks)
   int64_t colmin_begin; // first mp_minima column block (blocks only for an original t2)
   int64_t rowmin_begin; // first mp_minima row block, counted after all column blocks (original t1)
@@ -388,7 +389,8 @@ __global__ void __launch_bounds__(256) mp_prep_kernel(const MpFold *folds, int n
     cbs[tid] = k0 + tid < f.nv ? mm_dec(f.cb[k0 + tid]) : 0;
   }
   __syncthreads();
-  const int tk = k0 / kMpTile, kk0 = k0 % kMpTile;
+  const int bw = f.b_cols ? f.b_cols : kMpTile; // B rows: one 128-column tile, or a chain fold's whole row
+  const int tk = k0 / bw, kk0 = k0 % bw;
   const int sj = tid >> 3, kq = (tid & 7) * 4; // j sj, columns kq..kq+3
   int cbq[4];
 #pragma unroll
@@ -423,8 +425,8 @@ __global__ void __launch_bounds__(256) mp_prep_kernel(const MpFold *folds, int n
 #pragma unroll
     for (int q = 0; q < kMpPrepBatch; ++q)
       if (q < nb)
-        *reinterpret_cast<uint2 *>(f.B + (static_cast<int64_t>(tk) * f.nchunks + cb0 + q) * (kMpChunk * kMpTile) +
-                                   sj * kMpTile + kk0 + kq) = make_uint2(v[q][0] | (v[q][1] << 16), v[q][2] | (v[q][3] << 16));
+        *reinterpret_cast<uint2 *>(f.B + ((static_cast<int64_t>(tk) * f.nchunks + cb0 + q) * kMpChunk + sj) * bw + kk0 +
+                                   kq) = make_uint2(v[q][0] | (v[q][1] << 16), v[q][2] | (v[q][3] << 16));
   }
 }
 
@@ -661,6 +663,177 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
         }
       }
     }
+  }
+}
+
+// ---- mp_chain: a run of one-fold waves, row-parallel ---------------------------
+// A run of waves whose folds F_1 -> F_2 -> ... chain through t1 (F_{k+1}.t1 =
+// F_k.out) and whose t2 are all written before the run (config 5: 314 of its
+// 329 waves).  Eq. 2 works row by row, so each CTA carries R rows of the
+// source node through EVERY fold of the run with no grid-wide dependency:
+// per fold it normalises its rows of t1 (row minima over the full row, in the
+// CTA) into shared memory, streams the fold's whole B'' (packed once before the
+// run, [j][kMpChainCols] u16) through a bulk-copy ring fed by a producer warp
+// that runs ahead across fold boundaries, and writes out / argmins.  Each
+// consumer thread owns 4 columns (2 U16x2 pairs) of all R <= 8 rows.  Same
+// arithmetic, caps and keys as mp_fold.
+constexpr int kMpChainCols = 1024;                     // columns per B'' row (nv <= 1024)
+constexpr int kMpChainRows = 8;                        // rows per CTA at most
+constexpr int kMpChainJ = 16;                          // j per stage
+constexpr int kMpChainStages = 3;
+constexpr unsigned kMpChainStageBytes = kMpChainJ * kMpChainCols * 2; // 32 KiB
+constexpr int kMpChainNw = 1024;                       // padded nw at most (A in shared memory)
+constexpr size_t kMpChainSmem = kMpChainStages * kMpChainStageBytes + static_cast<size_t>(kMpChainNw) * kMpChainRows * 4 +
+                                2 * kMpChainStages * 8 + 64;
+
+template <int JB>
+__global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *folds, int K, int R) {
+  extern __shared__ __align__(128) unsigned char ch_smem[];
+  uint32_t *As = reinterpret_cast<uint32_t *>(ch_smem + kMpChainStages * kMpChainStageBytes); // [j][8] a'' (dup)
+  uint64_t *full = reinterpret_cast<uint64_t *>(As + kMpChainNw * kMpChainRows);
+  uint64_t *empty = full + kMpChainStages;
+  int *ras = reinterpret_cast<int *>(empty + kMpChainStages); // [8]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kMpChainStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kMpConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kMpConsumers / 32) { // producer: every fold's B'' stages, in order
+    if (lane == 0) {
+      int64_t nn = 0;
+      for (int k = 0; k < K; ++k) {
+        const MpFold &f = folds[k];
+        const int stages = f.nchunks * (kMpChunk / kMpChainJ);
+        for (int st = 0; st < stages; ++st, ++nn) {
+          const int s = static_cast<int>(nn % kMpChainStages);
+          mbar_wait(&empty[s], (static_cast<unsigned>(nn / kMpChainStages) & 1u) ^ 1u);
+          mbar_expect_tx(&full[s], kMpChainStageBytes);
+          bulk_g2s(ch_smem + s * kMpChainStageBytes, f.B + static_cast<int64_t>(st) * kMpChainJ * kMpChainCols,
+                   kMpChainStageBytes, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  constexpr uint32_t LOW2 = ((1u << JB) - 1) * 0x10001u;
+  constexpr int SPG = (1 << JB) >= kMpChainJ ? (1 << JB) / kMpChainJ : 1; // stages per argmin group
+  static_assert((1 << JB) >= kMpChainJ, "argmin groups span whole stages");
+  const int c4 = tid * 4; // this thread's columns c4..c4+3
+  int64_t nn = 0;
+  for (int k = 0; k < K; ++k) {
+    const MpFold &f = folds[k];
+    const int r0 = static_cast<int>(blockIdx.x) * R, nr = min(R, f.nu - r0);
+    const int nwp = f.nchunks * kMpChunk;
+    // ---- A: row minima of w + t1 over this CTA's rows, then a'' into shared memory
+    if (warp < nr) {
+      const int32_t *row = f.t1 + static_cast<int64_t>(r0 + warp) * f.nw;
+      int m = INT_MAX;
+      int j = lane;
+      for (; j + 96 < f.nw; j += 128) {
+        const int a0 = f.w[j] + row[j], a1 = f.w[j + 32] + row[j + 32];
+        const int a2 = f.w[j + 64] + row[j + 64], a3 = f.w[j + 96] + row[j + 96];
+        m = min(m, min(min(a0, a1), min(a2, a3)));
+      }
+      for (; j < f.nw; j += 32) m = min(m, f.w[j] + row[j]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) ras[warp] = m;
+    }
+    consumer_sync();
+    for (int x = tid; x < kMpChainRows * nwp; x += kMpConsumers) {
+      const int r = x / nwp, j = x - r * nwp;
+      uint32_t v = 0;
+      if (r < nr)
+        v = j < f.nw ? (static_cast<uint32_t>(min(f.w[j] + f.t1[static_cast<int64_t>(r0 + r) * f.nw + j] - ras[r], f.cap))
+                        << JB) | (static_cast<uint32_t>(j) & ((1u << JB) - 1))
+                     : 0xFFFFu;
+      As[j * kMpChainRows + r] = v * 0x10001u;
+    }
+    consumer_sync();
+    // ---- the fold: 8 rows x 2 column pairs per thread over all j
+    uint32_t key[kMpChainRows][4], m[kMpChainRows][2];
+#pragma unroll
+    for (int r = 0; r < kMpChainRows; ++r) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) key[r][q] = 0xFFFFFFFFu;
+      m[r][0] = m[r][1] = 0xFFFFFFFFu;
+    }
+    const int stages = nwp / kMpChainJ;
+    for (int st = 0; st < stages; ++st, ++nn) {
+      const int s = static_cast<int>(nn % kMpChainStages);
+      mbar_wait(&full[s], static_cast<unsigned>(nn / kMpChainStages) & 1u);
+      const uint32_t *Bs = reinterpret_cast<const uint32_t *>(ch_smem + s * kMpChainStageBytes) + tid * 2;
+      if (st % SPG == 0) {
+#pragma unroll
+        for (int r = 0; r < kMpChainRows; ++r) m[r][0] = m[r][1] = 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int jj = 0; jj < kMpChainJ; ++jj) {
+        const int j = st * kMpChainJ + jj;
+        uint32_t a[8];
+        *reinterpret_cast<uint4 *>(&a[0]) = *reinterpret_cast<const uint4 *>(As + j * kMpChainRows);
+        *reinterpret_cast<uint4 *>(&a[4]) = *reinterpret_cast<const uint4 *>(As + j * kMpChainRows + 4);
+        const uint2 b = *reinterpret_cast<const uint2 *>(Bs + jj * (kMpChainCols / 2));
+#pragma unroll
+        for (int r = 0; r < kMpChainRows; ++r) {
+          m[r][0] = __viaddmin_u16x2(a[r], b.x, m[r][0]);
+          m[r][1] = __viaddmin_u16x2(a[r], b.y, m[r][1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (st % SPG == SPG - 1 || st == stages - 1) {
+        const uint32_t G2 = static_cast<uint32_t>((st * kMpChainJ) >> JB) * ((1u << JB) * 0x10001u);
+#pragma unroll
+        for (int r = 0; r < kMpChainRows; ++r)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t gj = (m[r][q] & LOW2) | G2, mv = m[r][q] & ~LOW2;
+            key[r][2 * q] = min(key[r][2 * q], __byte_perm(mv, gj, 0x1054));
+            key[r][2 * q + 1] = min(key[r][2 * q + 1], __byte_perm(mv, gj, 0x3276));
+          }
+      }
+    }
+    // ---- epilogue: out = ra + cb + best, am = j
+    bool capped = false;
+    if (c4 < f.nv) {
+      int cbk[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cbk[q] = c4 + q < f.nv ? mm_dec(f.cb[c4 + q]) : 0;
+      const bool vec = c4 + 4 <= f.nv && (f.nv & 3) == 0;
+#pragma unroll
+      for (int r = 0; r < kMpChainRows; ++r) {
+        if (r >= nr) break;
+        int32_t ov[4];
+        uint16_t av[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int32_t best = static_cast<int32_t>(key[r][q] >> (16 + JB));
+          if (c4 + q < f.nv && best >= f.cap) capped = true;
+          ov[q] = ras[r] + cbk[q] + best;
+          av[q] = static_cast<uint16_t>(key[r][q] & 0xFFFFu);
+        }
+        int32_t *orow = f.out + static_cast<int64_t>(r0 + r) * f.nv + c4;
+        uint16_t *arow = f.am + static_cast<int64_t>(r0 + r) * f.nv + c4;
+        if (vec) {
+          *reinterpret_cast<int4 *>(orow) = *reinterpret_cast<const int4 *>(&ov[0]);
+          *reinterpret_cast<uint2 *>(arow) = *reinterpret_cast<const uint2 *>(&av[0]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c4 + q < f.nv) orow[q] = ov[q], arow[q] = av[q];
+        }
+      }
+    }
+    if (capped && f.ovf) atomicOr(f.ovf, 1u);
+    // the next fold reads this CTA's rows of out (its t1) from global memory
+    __threadfence_block();
+    consumer_sync();
   }
 }
 

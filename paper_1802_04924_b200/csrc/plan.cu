@@ -33,7 +33,7 @@ static int env_int(const char *name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 struct Knobs {
-  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_split_penalty_milli, merge_fuse,
+  int cluster, narrow_items, chain_smem_kb, chain_smem_big_kb, chain_big_gain, mp_chain, mp_chain_min, merge_fuse,
       chain_min_waves, early_build, grid_barrier, build_dynamic, panel,
       panel_side, chains,
       chain_path, rotate,
@@ -41,7 +41,8 @@ struct Knobs {
   Knobs()
       : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
         chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
-        chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), mp_split_penalty_milli(env_int("PARPLAN_MP_SPLIT_PENALTY", 250)),
+        chain_big_gain(env_int("PARPLAN_CHAIN_BIG_GAIN", 6)), mp_chain(env_int("PARPLAN_MP_CHAIN", 1)),
+        mp_chain_min(std::max(1, env_int("PARPLAN_MP_CHAIN_MIN", 4))),
         merge_fuse(env_int("PARPLAN_MERGE_FUSE", 1)), chain_min_waves(std::max(2, env_int("PARPLAN_CHAIN_MIN_WAVES", 2))),
         early_build(env_int("PARPLAN_EARLY_BUILD", 1)), grid_barrier(env_int("PARPLAN_GRID_BARRIER", 1)),
         build_dynamic(env_int("PARPLAN_BUILD_DYNAMIC", 1)),
@@ -333,7 +334,14 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   std::vector<int> mp_producer(static_cast<size_t>(E_total), -1); // large fold writing a table
   std::vector<char> mp_merge_out(static_cast<size_t>(E_total), 0); // table written by an mp_merge
   // persistent section: stream-K partial slots | counters (0 at rest) | ra, cb (0xFF.. before use)
-  size_t mp_bytes = 0, mp_part = 0, mp_cnt = 0, mp_ra = 0, mp_cb = 0;
+  size_t mp_bytes = 0, mp_part = 0, mp_cnt = 0, mp_ra = 0, mp_cb = 0, mp_chainb = 0;
+  struct MpRun {
+    int w0 = 0;
+    std::vector<int> ops;
+    int R = 1;
+  };
+  std::vector<MpRun> mp_runs;
+  std::vector<int> mp_run_of(s.ops.size(), -1);
   if constexpr (std::is_same_v<T, int32_t>) {
     std::vector<int64_t> R(static_cast<size_t>(E_total), 0), Kc(static_cast<size_t>(E_total), 0);
     for (int e = 0; e < t.ne; ++e) {
@@ -370,6 +378,55 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       at += align256(bytes);
       return o;
     };
+    // chain runs (minplus.cuh: mp_chain): consecutive one-fold waves whose
+    // folds chain through t1 and whose t2 exist before the run
+    if (!shard && kn.mp_chain) {
+      MpRun cur;
+      auto close = [&] {
+        if (static_cast<int>(cur.ops.size()) >= kn.mp_chain_min) mp_runs.push_back(cur);
+        cur = MpRun{};
+      };
+      for (int w = 1; w <= s.n_waves; ++w) {
+        const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
+        const int oi = s.exec[static_cast<size_t>(x0)];
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        const bool ok = x1 - x0 == 1 && large[static_cast<size_t>(oi)] && !op.type &&
+                        cols[static_cast<size_t>(op.e2)] <= kMpChainCols &&
+                        t.counts[static_cast<size_t>(op.removed)] <= kMpChainNw &&
+                        rows[static_cast<size_t>(op.e1)] <= kMpChainRows * ctx->sms;
+        if (!ok) {
+          close();
+          continue;
+        }
+        const bool extends = !cur.ops.empty() && op.e1 == s.ops[static_cast<size_t>(cur.ops.back())].ne &&
+                             prod_wave[static_cast<size_t>(op.e2)] < cur.w0;
+        if (!extends) {
+          close();
+          cur.w0 = w;
+        }
+        cur.ops.push_back(oi);
+      }
+      close();
+      for (size_t r = 0; r < mp_runs.size(); ++r)
+        for (int oi : mp_runs[r].ops) {
+          mp_run_of[static_cast<size_t>(oi)] = static_cast<int>(r);
+          // the run computes its row minima itself and feeds no column minima:
+          // consumers of its outputs run their own minima passes
+          mp_producer[static_cast<size_t>(s.ops[static_cast<size_t>(oi)].ne)] = -1;
+        }
+      for (MpRun &run : mp_runs) {
+        run.R = (rows[static_cast<size_t>(s.ops[static_cast<size_t>(run.ops[0])].e1)] + ctx->sms - 1) / ctx->sms;
+        for (int oi : run.ops) {
+          const Op &op = s.ops[static_cast<size_t>(oi)];
+          MpLayout &L = mpl[static_cast<size_t>(oi)];
+          L.nchunks = (t.counts[static_cast<size_t>(op.removed)] + kMpChunk - 1) / kMpChunk;
+          L.tiles_i = L.tiles_k = 1;
+          L.B = take(mp_chainb, static_cast<size_t>(L.nchunks) * kMpChunk * kMpChainCols * 2);
+          L.cb = take(mp_cb, static_cast<size_t>(cols[static_cast<size_t>(op.e2)]) * 4);
+          L.ra = take(mp_ra, 4);
+        }
+      }
+    }
     // per wave, in launch groups of at most kMpGroupBytes of operand blocks
     // (a wide wave — 471 folds of config 5 — would need 45 GB at C = 4096):
     // the operand blocks and tile counters (restored after every use) of one
@@ -381,7 +438,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       wave_group_jb[static_cast<size_t>(w)].assign(1, kMpOptJB);
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
-        if (!large[static_cast<size_t>(oi)]) continue;
+        if (!large[static_cast<size_t>(oi)] || mp_run_of[static_cast<size_t>(oi)] >= 0) continue;
         const Op &op = s.ops[static_cast<size_t>(oi)];
         MpLayout &L = mpl[static_cast<size_t>(oi)];
         const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)],
@@ -411,6 +468,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       mp_bytes = std::max(mp_bytes, off);
       mp_cnt = std::max(mp_cnt, coff);
     }
+    if (!mp_runs.empty()) {
+      PP_CUDA(cudaFuncSetAttribute(mp_chain_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpChainSmem)));
+      PP_CUDA(cudaFuncSetAttribute(mp_chain_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpChainSmem)));
+      PP_CUDA(cudaFuncSetAttribute(mp_chain_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpChainSmem)));
+    }
     if (mp_bytes) {
       mp_part = static_cast<size_t>(ctx->sms) * kMpTileCells * 4;
       // per device, every prepare (cheap; no process-wide cache across devices)
@@ -420,7 +482,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
     }
   }
-  const size_t mp_pbytes = mp_part + mp_cnt + mp_ra + mp_cb;
+  const size_t mp_pbytes = mp_part + mp_cnt + mp_ra + mp_cb + mp_chainb;
 
   const size_t tables_bytes =
       bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
@@ -597,6 +659,17 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   const int fused_nc = use_fused ? std::max(1, kn.cluster) : 1;
   const int64_t narrow_items = use_fused ? kn.narrow_items : 0;
   const size_t kChainSmemMax = static_cast<size_t>(kn.chain_smem_kb) * 1024;
+  // chain runs in the image: folds [p0, p0 + n) of mpf, B prep blocks, JB, cells, rows per CTA, first wave
+  struct RunImg {
+    size_t p0;
+    int n;
+    int64_t prep_blocks;
+    double cells;
+    int R, w0;
+    int jb = 6;
+    int nu = 0;
+  };
+  std::vector<RunImg> run_img;
   // sb: base of the device-only scratch section (buffers the kernels write:
   // enumeration block results, cost terms, stamps, chain path tables), not uploaded
   auto make_image = [&](unsigned char *db, unsigned char *sb) {
@@ -644,6 +717,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<MergeDesc<T>> merges;
     std::vector<MpFold> mpf;
     std::vector<MpMerge> mmv;
+    run_img.clear();
     int64_t colmin_blocks = 0, rowmin_blocks = 0; // mp_minima blocks over all large folds (one launch per plan)
     for (int w = 1; w <= EWn; ++w) {
       WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, {}, mmv.size(), 0, 0, {}};
@@ -686,6 +760,53 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
                                   static_cast<size_t>(blk(op.e2)) * cols[static_cast<size_t>(op.e2)] * sizeof(T));
         if (nu_eff(op.e1) == 0) continue; // no rows of this op on this rank
         if constexpr (std::is_same_v<T, int32_t>) {
+          if (large[static_cast<size_t>(oi)] && mp_run_of[static_cast<size_t>(oi)] >= 0) { // chain run member
+            const int ri = mp_run_of[static_cast<size_t>(oi)];
+            const MpRun &run = mp_runs[static_cast<size_t>(ri)];
+            const MpLayout &L = mpl[static_cast<size_t>(oi)];
+            unsigned char *pb = db + off_mpp;
+            if (oi == run.ops.front()) run_img.push_back(RunImg{mpf.size(), 0, 0, 0.0, run.R, w, 6, nu_eff(op.e1)});
+            RunImg &ri_ = run_img.back();
+            MpFold f{};
+            f.t1 = rowp(op.e1);
+            f.t2 = t2p(op.e2);
+            f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
+            f.out = out;
+            f.am = reinterpret_cast<uint16_t *>(db + off_am + am_off[static_cast<size_t>(oi)]);
+            f.cb = reinterpret_cast<uint32_t *>(pb + mp_part + mp_cnt + mp_ra + L.cb);
+            f.ra = reinterpret_cast<uint32_t *>(pb + mp_part + mp_cnt + L.ra);
+            f.B = reinterpret_cast<uint16_t *>(pb + mp_part + mp_cnt + mp_ra + mp_cb + L.B);
+            f.b_cols = kMpChainCols;
+            f.nu = nu_eff(op.e1);
+            f.nw = t.counts[static_cast<size_t>(op.removed)];
+            f.nv = cols[static_cast<size_t>(op.e2)];
+            f.tiles_i = f.tiles_k = 1;
+            f.nchunks = L.nchunks;
+            f.jb = fold_jb[static_cast<size_t>(oi)];
+            for (int o2 : run.ops) f.jb = std::min(f.jb, fold_jb[static_cast<size_t>(o2)]); // one JB per run
+            f.jb = std::max(f.jb, 4);
+            if (fold_opt[static_cast<size_t>(oi)]) {
+              f.cap = mp_max_cap(f.jb);
+              f.ovf = ovf_ptr();
+            } else {
+              f.cap = static_cast<int32_t>(fold_m[static_cast<size_t>(oi)] + 1);
+            }
+            PP_REQUIRE(((2 * int64_t(f.cap)) << f.jb) + (1 << f.jb) - 1 <= 65534, "min-plus operand cap exceeds 16 bits");
+            f.cb_ready = op.e2 < t.ne || mp_producer[static_cast<size_t>(op.e2)] >= 0 || mp_merge_out[static_cast<size_t>(op.e2)];
+            f.a_batches = 0; // the chain kernel normalises its own rows
+            f.b_batches = f.cb_ready ? (f.nchunks + kMpPrepBatch - 1) / kMpPrepBatch : 1;
+            f.prep_begin = ri_.prep_blocks;
+            ri_.prep_blocks += mp_prep_blocks(f);
+            f.colmin_begin = colmin_blocks;
+            if (op.e2 < t.ne) colmin_blocks += (f.nv + 31) / 32;
+            f.rowmin_begin = rowmin_blocks;
+            ri_.jb = f.jb;
+            ri_.cells += static_cast<double>(f.nu) * f.nw * f.nv;
+            ++ri_.n;
+            wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
+            mpf.push_back(f);
+            continue;
+          }
           if (large[static_cast<size_t>(oi)]) {
             const MpLayout &L = mpl[static_cast<size_t>(oi)];
             unsigned char *sb = db + off_mp, *pb = db + off_mpp;
@@ -1231,8 +1352,38 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       ++launches;
     }
   }
-  for (const auto &wr : im.waves) {
+  size_t next_run = 0;
+  for (size_t wi = 0; wi < im.waves.size(); ++wi) {
+    const auto &wr = im.waves[wi];
     if (use_fused) break;
+    if constexpr (std::is_same_v<T, int32_t>) {
+      if (next_run < run_img.size() && run_img[next_run].w0 == static_cast<int>(wi) + 1) { // a chain run starts here
+        const RunImg rn = run_img[next_run++];
+        const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + rn.p0;
+        const int64_t pb = rn.prep_blocks;
+        const int n = rn.n, R = rn.R, jb = rn.jb;
+        const int nu = rn.nu;
+        const unsigned grid = static_cast<unsigned>((nu + R - 1) / R);
+        P->steps.push_back([ctx, mf, n, pb](cudaStream_t st) { // every fold's B'' (and missing column minima)
+          mp_prep_kernel<<<static_cast<unsigned>(pb), 256, 0, st>>>(mf, n);
+          check_launch(ctx);
+        });
+        P->step_kind.push_back(6);
+        P->step_work.push_back(0.0);
+        P->steps.push_back([ctx, mf, n, R, grid, jb](cudaStream_t st) {
+          if (jb == 6)
+            mp_chain_kernel<6><<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
+          else if (jb == 5)
+            mp_chain_kernel<5><<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
+          else
+            mp_chain_kernel<4><<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
+          check_launch(ctx);
+        });
+        P->step_kind.push_back(17);
+        P->step_work.push_back(rn.cells);
+        launches += 2;
+      }
+    }
     push_gathers(wr.gathers);
     if (wr.nmm > 0) { // merges feeding large folds' t2 (independent of this wave's folds)
       const MpMerge *mm = reinterpret_cast<const MpMerge *>(dimg + im.oMM) + wr.mm0;

@@ -19,8 +19,8 @@ for C in [int(x) for x in sys.argv[1:]] or [1024]:
     by = {}
     for k, ms, w in prof:
         by[k] = by.get(k, 0.0) + ms
-    cells = sum(w for k, _, w in prof if k == "mp_fold")
-    fold_ms = by.get("mp_fold", 0.0)
+    cells = sum(w for k, _, w in prof if k in ("mp_fold", "mp_chain"))
+    fold_ms = by.get("mp_fold", 0.0) + by.get("mp_chain", 0.0)
     t0 = time.time()
     prep.launch()
     r2 = prep.fetch()
