@@ -680,13 +680,13 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
 constexpr int kMpChainCols = 1024;                     // columns per B'' row (nv <= 1024)
 constexpr int kMpChainRows = 8;                        // rows per CTA at most
 constexpr int kMpChainJ = 16;                          // j per stage
-constexpr int kMpChainStages = 3;
+constexpr int kMpChainStages = 5;
 constexpr unsigned kMpChainStageBytes = kMpChainJ * kMpChainCols * 2; // 32 KiB
 constexpr int kMpChainNw = 1024;                       // padded nw at most (A in shared memory)
 constexpr size_t kMpChainSmem = kMpChainStages * kMpChainStageBytes + static_cast<size_t>(kMpChainNw) * kMpChainRows * 4 +
                                 2 * kMpChainStages * 8 + 64;
 
-template <int JB>
+template <int JB, int RR> // RR: rows per CTA computed (>= R; the unrolled register tile)
 __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *folds, int K, int R) {
   extern __shared__ __align__(128) unsigned char ch_smem[];
   uint32_t *As = reinterpret_cast<uint32_t *>(ch_smem + kMpChainStages * kMpChainStageBytes); // [j][8] a'' (dup)
@@ -729,36 +729,36 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
     const MpFold &f = folds[k];
     const int r0 = static_cast<int>(blockIdx.x) * R, nr = min(R, f.nu - r0);
     const int nwp = f.nchunks * kMpChunk;
-    // ---- A: row minima of w + t1 over this CTA's rows, then a'' into shared memory
+    // ---- A: one warp per row loads the row once (all loads in flight), takes
+    // its minimum and writes a'' into shared memory (rows >= nr are never stored)
     if (warp < nr) {
+      constexpr int kPer = kMpChainNw / 32;
       const int32_t *row = f.t1 + static_cast<int64_t>(r0 + warp) * f.nw;
+      int v[kPer];
       int m = INT_MAX;
-      int j = lane;
-      for (; j + 96 < f.nw; j += 128) {
-        const int a0 = f.w[j] + row[j], a1 = f.w[j + 32] + row[j + 32];
-        const int a2 = f.w[j + 64] + row[j + 64], a3 = f.w[j + 96] + row[j + 96];
-        m = min(m, min(min(a0, a1), min(a2, a3)));
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int j = i * 32 + lane;
+        v[i] = j < f.nw ? f.w[j] + row[j] : INT_MAX;
+        m = min(m, v[i]);
       }
-      for (; j < f.nw; j += 32) m = min(m, f.w[j] + row[j]);
 #pragma unroll
       for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
       if (lane == 0) ras[warp] = m;
-    }
-    consumer_sync();
-    for (int x = tid; x < kMpChainRows * nwp; x += kMpConsumers) {
-      const int r = x / nwp, j = x - r * nwp;
-      uint32_t v = 0;
-      if (r < nr)
-        v = j < f.nw ? (static_cast<uint32_t>(min(f.w[j] + f.t1[static_cast<int64_t>(r0 + r) * f.nw + j] - ras[r], f.cap))
-                        << JB) | (static_cast<uint32_t>(j) & ((1u << JB) - 1))
-                     : 0xFFFFu;
-      As[j * kMpChainRows + r] = v * 0x10001u;
-    }
-    consumer_sync();
-    // ---- the fold: 8 rows x 2 column pairs per thread over all j
-    uint32_t key[kMpChainRows][4], m[kMpChainRows][2];
 #pragma unroll
-    for (int r = 0; r < kMpChainRows; ++r) {
+      for (int i = 0; i < kPer; ++i) {
+        const int j = i * 32 + lane;
+        if (j < nwp)
+          As[j * kMpChainRows + warp] =
+              (j < f.nw ? (static_cast<uint32_t>(min(v[i] - m, f.cap)) << JB) | (static_cast<uint32_t>(j) & ((1u << JB) - 1))
+                        : 0xFFFFu) * 0x10001u;
+      }
+    }
+    consumer_sync();
+    // ---- the fold: RR rows x 2 column pairs per thread over all j
+    uint32_t key[RR][4], m[RR][2];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) key[r][q] = 0xFFFFFFFFu;
       m[r][0] = m[r][1] = 0xFFFFFFFFu;
@@ -770,17 +770,17 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
       const uint32_t *Bs = reinterpret_cast<const uint32_t *>(ch_smem + s * kMpChainStageBytes) + tid * 2;
       if (st % SPG == 0) {
 #pragma unroll
-        for (int r = 0; r < kMpChainRows; ++r) m[r][0] = m[r][1] = 0xFFFFFFFFu;
+        for (int r = 0; r < RR; ++r) m[r][0] = m[r][1] = 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int jj = 0; jj < kMpChainJ; ++jj) {
         const int j = st * kMpChainJ + jj;
         uint32_t a[8];
         *reinterpret_cast<uint4 *>(&a[0]) = *reinterpret_cast<const uint4 *>(As + j * kMpChainRows);
-        *reinterpret_cast<uint4 *>(&a[4]) = *reinterpret_cast<const uint4 *>(As + j * kMpChainRows + 4);
+        if constexpr (RR > 4) *reinterpret_cast<uint4 *>(&a[4]) = *reinterpret_cast<const uint4 *>(As + j * kMpChainRows + 4);
         const uint2 b = *reinterpret_cast<const uint2 *>(Bs + jj * (kMpChainCols / 2));
 #pragma unroll
-        for (int r = 0; r < kMpChainRows; ++r) {
+        for (int r = 0; r < RR; ++r) {
           m[r][0] = __viaddmin_u16x2(a[r], b.x, m[r][0]);
           m[r][1] = __viaddmin_u16x2(a[r], b.y, m[r][1]);
         }
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
       if (st % SPG == SPG - 1 || st == stages - 1) {
         const uint32_t G2 = static_cast<uint32_t>((st * kMpChainJ) >> JB) * ((1u << JB) * 0x10001u);
 #pragma unroll
-        for (int r = 0; r < kMpChainRows; ++r)
+        for (int r = 0; r < RR; ++r)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const uint32_t gj = (m[r][q] & LOW2) | G2, mv = m[r][q] & ~LOW2;
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
       for (int q = 0; q < 4; ++q) cbk[q] = c4 + q < f.nv ? mm_dec(f.cb[c4 + q]) : 0;
       const bool vec = c4 + 4 <= f.nv && (f.nv & 3) == 0;
 #pragma unroll
-      for (int r = 0; r < kMpChainRows; ++r) {
+      for (int r = 0; r < RR; ++r) {
         if (r >= nr) break;
         int32_t ov[4];
         uint16_t av[4];

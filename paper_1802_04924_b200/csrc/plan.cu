@@ -165,6 +165,23 @@ struct StageClock {
   }
 };
 
+using MpChainFn = void (*)(const MpFold *, int, int);
+// the chain kernel for a run: optimistic runs (JB 6) get the exact row count
+// per CTA, proven-cap runs (JB <= 5) the 8-row tile
+static MpChainFn mp_chain_launch(int jb, int R) {
+  if (jb < 6) return jb == 5 ? mp_chain_kernel<5, 8> : mp_chain_kernel<4, 8>;
+  switch (R) {
+  case 1: return mp_chain_kernel<6, 1>;
+  case 2: return mp_chain_kernel<6, 2>;
+  case 3: return mp_chain_kernel<6, 3>;
+  case 4: return mp_chain_kernel<6, 4>;
+  case 5: return mp_chain_kernel<6, 5>;
+  case 6: return mp_chain_kernel<6, 6>;
+  case 7: return mp_chain_kernel<6, 7>;
+  default: return mp_chain_kernel<6, 8>;
+  }
+}
+
 template <class T>
 static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   StageClock clk;
@@ -468,11 +485,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       mp_bytes = std::max(mp_bytes, off);
       mp_cnt = std::max(mp_cnt, coff);
     }
-    if (!mp_runs.empty()) {
-      PP_CUDA(cudaFuncSetAttribute(mp_chain_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpChainSmem)));
-      PP_CUDA(cudaFuncSetAttribute(mp_chain_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpChainSmem)));
-      PP_CUDA(cudaFuncSetAttribute(mp_chain_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpChainSmem)));
-    }
+    if (!mp_runs.empty())
+      for (const MpRun &run : mp_runs) // per device, every prepare (cheap)
+        for (int jb : {4, 5, 6})
+          PP_CUDA(cudaFuncSetAttribute(mp_chain_launch(jb, run.R), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kMpChainSmem)));
     if (mp_bytes) {
       mp_part = static_cast<size_t>(ctx->sms) * kMpTileCells * 4;
       // per device, every prepare (cheap; no process-wide cache across devices)
@@ -1371,12 +1388,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         P->step_kind.push_back(6);
         P->step_work.push_back(0.0);
         P->steps.push_back([ctx, mf, n, R, grid, jb](cudaStream_t st) {
-          if (jb == 6)
-            mp_chain_kernel<6><<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
-          else if (jb == 5)
-            mp_chain_kernel<5><<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
-          else
-            mp_chain_kernel<4><<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
+          mp_chain_launch(jb, R)<<<grid, kMpThreads, kMpChainSmem, st>>>(mf, n, R);
           check_launch(ctx);
         });
         P->step_kind.push_back(17);
