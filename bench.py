@@ -409,6 +409,48 @@ def minplus_point(P, ctx, stream, C, runs, check):
     return out
 
 
+def minplus_fp64(P, ctx, stream, C, check):
+    """The FP64 large-table fold (minplus64.cuh) on the config-5 graph with
+    non-dyadic FP64 tables (what measured costs look like; the fixed-point
+    certificate rejects them): cells/s against the FP64-pipe roofline
+    (64 DADD lane-ops/clk/SM measured, profiles/r02_microbench_fp64_tput.log;
+    2 FP64-pipe ops per cell: DADD + DSETP)."""
+    import torch
+
+    g = P.series_parallel_graph(1, 1000, 0.3)
+    t = P.synthetic_cost_tables64(g, C, seed=1, ctx=ctx)
+    prep = P.PreparedPlan(g, tables=t, ctx=ctx)
+    prep.launch()
+    r = prep.fetch()
+    prof = prep.profile()
+    fold_ms = sum(ms for k, ms, _ in prof if k == "mp64_fold")
+    cells = sum(w for k, _, w in prof if k == "mp64_fold")
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s0.record(stream)
+    prep.launch()
+    s1.record(stream)
+    prep.fetch()
+    plan_ms = s0.elapsed_time(s1)
+    del prep
+    peak = 148 * 32 * 1965e6
+    out = {"configs": C, "tables": "device generator, FP64 (k + u)/64, 53-bit u (uncertified)", "precision": r.precision,
+           "fold_kernel_ms": fold_ms, "cell_updates": cells, "cell_updates_per_s": cells / (fold_ms * 1e-3) if fold_ms else None,
+           "fp64_cell_peak_per_s": peak, "fold_frac": cells / (fold_ms * 1e-3) / peak if fold_ms else None,
+           "peak_basis": "148 SM x 64 FP64 lane-ops/clk (measured) / 2 ops per cell x 1965 MHz",
+           "plan_ms": plan_ms, "cost": r.cost}
+    if check:
+        ctx.set_kernel_policy("generic")
+        try:
+            b = P.plan_with_tables(g, t)
+            out["matches_generic"] = bool(list(b.indices) == list(r.indices) and b.cost == r.cost)
+            out["generic_ms"] = b.device_ms
+        finally:
+            ctx.set_kernel_policy("auto")
+    del t
+    return out
+
+
 def minplus(P, ctx, args, stream, sm_mhz):
     """Min-plus sweep; the headline roofline is the C=1024 point's mp_fold_kernel."""
     points = {}
@@ -420,10 +462,15 @@ def minplus(P, ctx, args, stream, sm_mhz):
     f_mhz = sm_mhz or peaks().get("sm_max_mhz", 1965.0)
     peak_tflops = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # FP32 CUDA-core: 2 ops (add + min) per cell update per lane-clock
     for pt in points.values():
-        if "fold_kernel_ms" in pt and pt["fold_kernel_ms"]:
+        if "fold_kernel_ms" in pt and pt["fold_kernel_ms"] and pt.get("precision") != "fp64":
             pt["fold_frac"] = 2.0 * pt["cell_updates"] / (pt["fold_kernel_ms"] * 1e-3) / 1e12 / peak_tflops
             pt["plan_frac"] = 2.0 * pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3) / 1e12 / peak_tflops
             pt["plan_cell_updates_per_s"] = pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3)
+    if args.fp64_c:
+        try:
+            points[f"fp64_{args.fp64_c}"] = minplus_fp64(P, ctx, stream, args.fp64_c, check=not args.no_check)
+        except Exception as exc:
+            points[f"fp64_{args.fp64_c}"] = {"error": str(exc)[:300]}
     head = points.get(str(args.minplus_c)) or next(iter(points.values()), {})
     traffic, basis = committed_traffic("mp_fold_kernel")
     roof = None
@@ -618,7 +665,7 @@ def run_ours(args):
             f = mc["sm_mhz"]
             pk = 148 * 128 * 2 * f * 1e6 / 1e12
             for pt in points.values():
-                if pt.get("fold_kernel_ms"):
+                if pt.get("fold_kernel_ms") and pt.get("precision") != "fp64":
                     pt["fold_frac"] = 2.0 * pt["cell_updates"] / (pt["fold_kernel_ms"] * 1e-3) / 1e12 / pk
                     pt["plan_frac"] = 2.0 * pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3) / 1e12 / pk
             if roof:
@@ -677,6 +724,7 @@ def main():
     ap.add_argument("--minplus-sweep", type=lambda x: [int(c) for c in x.split(",") if c], default=[1024, 2048, 4096])
     ap.add_argument("--minplus-runs", type=int, default=2)
     ap.add_argument("--no-check", action="store_true", help="skip the min-plus parity checks")
+    ap.add_argument("--fp64-c", type=int, default=1024, help="configs of the FP64 large-fold point (0: skip)")
     ap.add_argument("--quick", action="store_true", help="headline only (no model sweep / drop-in / K1)")
     ap.add_argument("--shard-c", type=int, default=4096, help="N > 1: configs of the row-sharded min-plus plan")
     ap.add_argument("--no-shard", action="store_true", help="N > 1: skip the row-sharded plans")

@@ -218,6 +218,10 @@ pp_status pp_tables_upload(pp_context *ctx, const pp_graph *g, const int32_t *co
  * host generator cannot feed): catalogs {1,1,1,i+1} i<configs, values
  * k/64, k = splitmix64(seed, table, cell) % 641. */
 pp_status pp_tables_synthetic(pp_context *ctx, const pp_graph *g, int32_t configs, uint64_t seed, pp_tables **out);
+/* FP64 variant (values (k + u) / 64 with a 53-bit fraction u: rejected by the
+ * fixed-point certificate, like measured costs): exercises the FP64 large-table
+ * fold (minplus64.cuh). */
+pp_status pp_tables_synthetic64(pp_context *ctx, const pp_graph *g, int32_t configs, uint64_t seed, pp_tables **out);
 pp_status pp_tables_destroy(pp_tables *t);
 /* counts[n_layers]; xfer_cells = sum over edges of count(src)*count(dst) */
 pp_status pp_tables_counts(const pp_tables *t, int32_t *counts, int64_t *xfer_cells);

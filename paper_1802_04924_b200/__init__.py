@@ -31,5 +31,6 @@ from .capi import (  # noqa: F401
     series_parallel_graph,
     synthetic_instance,
     synthetic_cost_tables,
+    synthetic_cost_tables64,
     upload_cost_tables,
 )

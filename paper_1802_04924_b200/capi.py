@@ -108,6 +108,7 @@ _SIGS = {
     "pp_tables_build": (C.c_int, [_vp, _vp, C.POINTER(_DeviceDesc), _pp]),
     "pp_tables_upload": (C.c_int, [_vp, _vp, _i32p, _vp, _f64p, _f64p, _pp]),
     "pp_tables_synthetic": (C.c_int, [_vp, _vp, C.c_int32, C.c_uint64, _pp]),
+    "pp_tables_synthetic64": (C.c_int, [_vp, _vp, C.c_int32, C.c_uint64, _pp]),
     "pp_tables_destroy": (C.c_int, [_vp]),
     "pp_tables_counts": (C.c_int, [_vp, _vp, C.POINTER(C.c_int64)]),
     "pp_tables_download": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
@@ -511,6 +512,14 @@ def random_series_parallel_graph(seed: int, node_count: int = 6, max_configs: in
     return graph, CostTables(ctx, graph, t)
 
 
+def synthetic_cost_tables64(graph: ComputationGraph, configs: int, seed: int, ctx: Optional[Context] = None) -> CostTables:
+    """FP64 config-5 tables (non-dyadic values; the FP64 large-table fold)."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(lib().pp_tables_synthetic64(ctx.h, graph.h, configs, seed, C.byref(h)))
+    return CostTables(ctx, graph, h)
+
+
 def synthetic_instance(seed: int, node_count: int, configs: int, bp: float = 0.3, ctx: Optional[Context] = None):
     """Config-5 generator (reference draw order, C dummy configs per layer) -> (graph, device tables)."""
     ctx = ctx or default_context()
@@ -623,7 +632,7 @@ class PreparedPlan:
         names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h", 5: "memset", 6: "mp_prep",
                  7: "mp_minima", 8: "mp_fold", 9: "mp_merge", 10: "fused", 11: "fused.tables",
                  12: "fused.wave", 13: "fused.enumerate", 14: "fused.finish", 15: "allgather", 16: "fused.chain",
-                 17: "mp_chain"}
+                 17: "mp_chain", 18: "mp64_fold"}
         return [(names[int(k)], float(m), float(w)) for k, m, w in zip(kind, ms, work)]
 
     def __del__(self):

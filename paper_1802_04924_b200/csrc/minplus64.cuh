@@ -1,0 +1,166 @@
+// minplus64.cuh — the large-table Eq. 2 fold for FP64 tables (analytic or
+// measured costs that the fixed-point certificate rejects).
+//
+// cand = (w[j] + t1[i][j]) + t2[j][k] in the reference's summation order
+// (planner.hpp:139-155): the first add is done once per (i, j) in the prep
+// (the same IEEE rounding), the second per cell; strict '<' over ascending j
+// keeps the lowest index among equal candidates.  64x64 output tile per CTA,
+// 4x4 cells per thread: per j, 16 DADD + 16 DSETP on the FP64 pipe and three
+// selects per cell (value halves and j); operands staged by bulk copies
+// (thread 0, mbarrier ring) from per-(tile, 32-j chunk) contiguous blocks.
+//
+//   mp64_prep  a = w + t1 -> A [tile_i][chunk][32 j][64 i]  (+inf for padded j)
+//              t2         -> B [tile_k][chunk][32 j][64 k]  (0 for padded j)
+//   mp64_fold  one CTA per (fold, tile), all chunks; out, argmin
+#pragma once
+
+#include "kernels.cuh"
+
+#include <cstdint>
+
+namespace pp {
+
+constexpr int kMp64Tile = 64;
+constexpr int kMp64Chunk = 32;
+constexpr int kMp64Stages = 3;
+constexpr int kMp64Threads = 256;
+constexpr int kMp64MinSide = 512; // folds with nu, nv >= this take mp64 (per-wave executor)
+constexpr unsigned kMp64StageA = kMp64Chunk * kMp64Tile * 8; // 16 KiB
+constexpr unsigned kMp64StageBytes = 2 * kMp64StageA;
+constexpr size_t kMp64Smem = kMp64Stages * kMp64StageBytes + 2 * kMp64Stages * 8;
+
+struct Mp64Fold {
+  const double *t1, *t2, *w;
+  double *out;
+  uint16_t *am;
+  double *A, *B;
+  int32_t nu, nw, nv, tiles_i, tiles_k, nchunks;
+  int64_t prep_begin; // A prep blocks (row groups of 32), then B prep blocks (chunk rows)
+  int32_t prep_a;
+  int64_t tile_begin; // first mp64_fold block
+};
+
+__device__ __forceinline__ int find64(const Mp64Fold *d, int n, int64_t b, bool tiles) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((tiles ? d[mid].tile_begin : d[mid].prep_begin) <= b)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// A block: 32 rows x all chunks (32x32 tiles through shared memory, transposed);
+// B block: one 32-j chunk row of t2 for all column tiles.
+__global__ void __launch_bounds__(256) mp64_prep_kernel(const Mp64Fold *folds, int n) {
+  const int64_t b = blockIdx.x;
+  const Mp64Fold &f = folds[find64(folds, n, b, false)];
+  const int64_t pb = b - f.prep_begin;
+  const int tid = threadIdx.x;
+  if (pb < f.prep_a) {
+    __shared__ double tr[32][33];
+    const int i0 = static_cast<int>(pb) * 32, ti = i0 / kMp64Tile, ii0 = i0 % kMp64Tile;
+    const int lr = tid >> 3, lj = (tid & 7) * 4; // load: row lr, j lj..lj+3
+    const int sj = tid >> 3, sr = (tid & 7) * 4; // store: j sj, rows sr..sr+3
+    const int i = i0 + lr;
+    for (int c = 0; c < f.nchunks; ++c) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = c * kMp64Chunk + lj + e;
+        tr[lj + e][lr] = i < f.nu && j < f.nw ? f.w[j] + f.t1[static_cast<int64_t>(i) * f.nw + j] // reference: w + t1 first
+                                              : __longlong_as_double(0x7ff0000000000000LL);        // +inf: never a minimum
+      }
+      __syncthreads();
+      double *dst = f.A + (static_cast<int64_t>(ti) * f.nchunks + c) * (kMp64Chunk * kMp64Tile) + sj * kMp64Tile + ii0 + sr;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = tr[sj][sr + e];
+      __syncthreads();
+    }
+    return;
+  }
+  const int64_t bb = pb - f.prep_a; // chunk c: rows j of all column tiles
+  const int c = static_cast<int>(bb);
+  for (int x = tid; x < kMp64Chunk * f.tiles_k * kMp64Tile; x += 256) {
+    const int jj = x / (f.tiles_k * kMp64Tile), k = x - jj * (f.tiles_k * kMp64Tile);
+    const int j = c * kMp64Chunk + jj, tk = k / kMp64Tile;
+    f.B[(static_cast<int64_t>(tk) * f.nchunks + c) * (kMp64Chunk * kMp64Tile) + jj * kMp64Tile + (k - tk * kMp64Tile)] =
+        j < f.nw && k < f.nv ? f.t2[static_cast<int64_t>(j) * f.nv + k] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kMp64Threads, 2) mp64_fold_kernel(const Mp64Fold *folds, int n) {
+  extern __shared__ __align__(128) unsigned char m64_smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(m64_smem + kMp64Stages * kMp64StageBytes);
+  const int64_t b = blockIdx.x;
+  const Mp64Fold &f = folds[find64(folds, n, b, true)];
+  const int tile = static_cast<int>(b - f.tile_begin);
+  const int ti = tile / f.tiles_k, tk = tile % f.tiles_k;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kMp64Stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double *Ab = f.A + static_cast<int64_t>(ti) * f.nchunks * (kMp64Chunk * kMp64Tile);
+  const double *Bb = f.B + static_cast<int64_t>(tk) * f.nchunks * (kMp64Chunk * kMp64Tile);
+  auto issue = [&](int c) {
+    const int s = c % kMp64Stages;
+    unsigned char *st = m64_smem + s * kMp64StageBytes;
+    mbar_expect_tx(&full[s], kMp64StageBytes);
+    bulk_g2s(st, Ab + static_cast<int64_t>(c) * (kMp64Chunk * kMp64Tile), kMp64StageA, &full[s]);
+    bulk_g2s(st + kMp64StageA, Bb + static_cast<int64_t>(c) * (kMp64Chunk * kMp64Tile), kMp64StageA, &full[s]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < kMp64Stages - 1 && c < f.nchunks; ++c) issue(c);
+  double best[4][4];
+  int bj[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) best[r][q] = __longlong_as_double(0x7ff0000000000000LL), bj[r][q] = 0;
+  for (int c = 0; c < f.nchunks; ++c) {
+    const int s = c % kMp64Stages;
+    // the stage refilled below was last read in iteration c - 1: every thread is past it
+    __syncthreads();
+    if (tid == 0 && c + kMp64Stages - 1 < f.nchunks) {
+      fence_proxy_async(); // generic reads of that stage before the async writes
+      issue(c + kMp64Stages - 1);
+    }
+    mbar_wait(&full[s], static_cast<unsigned>(c / kMp64Stages) & 1u);
+    const double *As = reinterpret_cast<const double *>(m64_smem + s * kMp64StageBytes) + ty * 4;
+    const double *Bs = reinterpret_cast<const double *>(m64_smem + s * kMp64StageBytes + kMp64StageA) + tx * 4;
+#pragma unroll 8
+    for (int jj = 0; jj < kMp64Chunk; ++jj) {
+      double a[4], bv[4];
+      *reinterpret_cast<double2 *>(&a[0]) = *reinterpret_cast<const double2 *>(As + jj * kMp64Tile);
+      *reinterpret_cast<double2 *>(&a[2]) = *reinterpret_cast<const double2 *>(As + jj * kMp64Tile + 2);
+      *reinterpret_cast<double2 *>(&bv[0]) = *reinterpret_cast<const double2 *>(Bs + jj * kMp64Tile);
+      *reinterpret_cast<double2 *>(&bv[2]) = *reinterpret_cast<const double2 *>(Bs + jj * kMp64Tile + 2);
+      const int j = c * kMp64Chunk + jj;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double cand = __dadd_rn(a[r], bv[q]);
+          if (cand < best[r][q]) best[r][q] = cand, bj[r][q] = j; // strict: the lowest j wins ties
+        }
+    }
+  }
+  const int i0 = ti * kMp64Tile + ty * 4, k0 = tk * kMp64Tile + tx * 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = i0 + r;
+    if (i >= f.nu) break;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k0 + q < f.nv) {
+        f.out[static_cast<int64_t>(i) * f.nv + k0 + q] = best[r][q];
+        f.am[static_cast<int64_t>(i) * f.nv + k0 + q] = static_cast<uint16_t>(bj[r][q]);
+      }
+  }
+}
+
+} // namespace pp

@@ -13,6 +13,7 @@
 #include "fused.cuh"
 #include "kernels.cuh"
 #include "minplus.cuh"
+#include "minplus64.cuh"
 
 #include <array>
 #include <algorithm>
@@ -499,6 +500,40 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
     }
   }
+  // ---- large FP64 folds (minplus64.cuh): per wave, launch groups of operand blocks
+  std::vector<char> large64(s.ops.size(), 0);
+  std::vector<int> mp64_group(s.ops.size(), 0);
+  std::vector<std::array<size_t, 2>> mp64_off(s.ops.size(), {0, 0}); // A, B in the per-wave section
+  if constexpr (std::is_same_v<T, double>) {
+    constexpr size_t kGroupBytes = size_t(2) << 30;
+    for (int w = 1; w <= s.n_waves; ++w) {
+      size_t off = 0;
+      int g = 0;
+      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
+        const int oi = s.exec[static_cast<size_t>(x)];
+        const Op &op = s.ops[static_cast<size_t>(oi)];
+        if (op.type || ctx->no_minplus) continue;
+        const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)], nv = cols[static_cast<size_t>(op.e2)];
+        // below ~512 rows / columns a wave holds too few 64x64 tiles: the generic kernels win
+        if (nu < kMp64MinSide || nv < kMp64MinSide || nw < kMp64Chunk * 2) continue;
+        large64[static_cast<size_t>(oi)] = 1;
+        const int nch = (nw + kMp64Chunk - 1) / kMp64Chunk;
+        const size_t a = align256(static_cast<size_t>((nu + kMp64Tile - 1) / kMp64Tile) * nch * kMp64StageA);
+        const size_t b = align256(static_cast<size_t>((nv + kMp64Tile - 1) / kMp64Tile) * nch * kMp64StageA);
+        if (off > 0 && off + a + b > kGroupBytes) {
+          mp_bytes = std::max(mp_bytes, off);
+          off = 0;
+          ++g;
+        }
+        mp64_group[static_cast<size_t>(oi)] = g;
+        mp64_off[static_cast<size_t>(oi)] = {off, off + a};
+        off += a + b;
+      }
+      mp_bytes = std::max(mp_bytes, off);
+    }
+    if (mp_bytes)
+      PP_CUDA(cudaFuncSetAttribute(mp64_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMp64Smem)));
+  }
   const size_t mp_pbytes = mp_part + mp_cnt + mp_ra + mp_cb + mp_chainb;
 
   const size_t tables_bytes =
@@ -538,6 +573,13 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       double cells = 0.0;
     };
     std::vector<MpGroup> mg;
+    struct Mp64Group {
+      size_t p0 = 0; // FP64 large folds [p0, p0 + np) in m64
+      int np = 0;
+      int64_t prep_blocks = 0, tiles = 0;
+      double cells = 0.0;
+    };
+    std::vector<Mp64Group> mg64;
     size_t mm0 = 0; // min-plus merges: [mm0, mm0 + nmm) in mmv
     int nmm = 0;
     int64_t mm_blocks = 0;
@@ -560,10 +602,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     int nG;
     size_t res_bytes;
     size_t oMM = 0;            // min-plus merges (all waves)
+    size_t oM64 = 0;           // FP64 large folds (all waves)
     int n_mp = 0;              // large folds (all waves)
     int64_t colmin_blocks = 0, rowmin_blocks = 0; // mp_minima blocks
   };
-  const bool use_fused = mp_bytes == 0 && !ctx->no_fused && !shard;
+  const bool use_fused = mp_bytes == 0 && mp_pbytes == 0 && !ctx->no_fused && !shard; // no large (U16 or FP64) folds
   // ---- effective schedule of the fused kernel: merge absorption ------------
   // An edge elimination (Eq. 3, out = a + b) whose operand a comes from a fold
   // F (or from merges already absorbed into F) while b is ready before F runs
@@ -733,11 +776,12 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     std::vector<FoldOps> fold_ops;
     std::vector<MergeDesc<T>> merges;
     std::vector<MpFold> mpf;
+    std::vector<Mp64Fold> m64;
     std::vector<MpMerge> mmv;
     run_img.clear();
     int64_t colmin_blocks = 0, rowmin_blocks = 0; // mp_minima blocks over all large folds (one launch per plan)
     for (int w = 1; w <= EWn; ++w) {
-      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, {}, mmv.size(), 0, 0, {}};
+      WaveRange wr{folds.size(), merges.size(), 0, 0, 0, 0, 0.0, {}, {}, mmv.size(), 0, 0, {}};
       // a wave whose generic folds cover fewer than 2 x SMs 32x32 tiles uses
       // 16x16 tiles: 4x the blocks, a quarter of the per-tile latency
       int64_t big_tiles = 0;
@@ -888,6 +932,38 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             G.units += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.nchunks;
             G.cells += static_cast<double>(f.nu) * f.nw * f.nv;
             mpf.push_back(f);
+            ++G.np;
+            continue;
+          }
+        }
+        if constexpr (std::is_same_v<T, double>) {
+          if (large64[static_cast<size_t>(oi)]) {
+            const int gi = mp64_group[static_cast<size_t>(oi)];
+            if (static_cast<int>(wr.mg64.size()) <= gi) wr.mg64.resize(static_cast<size_t>(gi) + 1);
+            auto &G = wr.mg64[static_cast<size_t>(gi)];
+            if (G.np == 0) G.p0 = m64.size();
+            Mp64Fold f{};
+            f.t1 = rowp(op.e1);
+            f.t2 = t2p(op.e2);
+            f.w = onode + t.cat_off[static_cast<size_t>(op.removed)];
+            f.out = out;
+            f.am = amp(oi);
+            f.A = reinterpret_cast<double *>(db + off_mp + mp64_off[static_cast<size_t>(oi)][0]);
+            f.B = reinterpret_cast<double *>(db + off_mp + mp64_off[static_cast<size_t>(oi)][1]);
+            f.nu = nu_eff(op.e1);
+            f.nw = t.counts[static_cast<size_t>(op.removed)];
+            f.nv = cols[static_cast<size_t>(op.e2)];
+            f.tiles_i = (f.nu + kMp64Tile - 1) / kMp64Tile;
+            f.tiles_k = (f.nv + kMp64Tile - 1) / kMp64Tile;
+            f.nchunks = (f.nw + kMp64Chunk - 1) / kMp64Chunk;
+            f.prep_a = (f.nu + 31) / 32;
+            f.prep_begin = G.prep_blocks;
+            G.prep_blocks += f.prep_a + f.nchunks;
+            f.tile_begin = G.tiles;
+            G.tiles += static_cast<int64_t>(f.tiles_i) * f.tiles_k;
+            G.cells += static_cast<double>(f.nu) * f.nw * f.nv;
+            wr.cells += static_cast<double>(f.nu) * f.nw * f.nv;
+            m64.push_back(f);
             ++G.np;
             continue;
           }
@@ -1171,6 +1247,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     im.oT = scr(static_cast<size_t>(t.nl + t.ne) * sizeof(double));
     im.oMP = pk.put(mpf);
     im.oMM = pk.put(mmv);
+    im.oM64 = pk.put(m64);
     im.n_mp = static_cast<int>(mpf.size());
     im.colmin_blocks = colmin_blocks;
     im.rowmin_blocks = rowmin_blocks;
@@ -1409,6 +1486,25 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       P->step_kind.push_back(9);
       P->step_work.push_back(wr.mm_cells);
       ++launches;
+    }
+    for (const auto &grp : wr.mg64) { // large FP64 folds of this wave, per launch group: prep -> tile fold
+      const Mp64Fold *mf = reinterpret_cast<const Mp64Fold *>(dimg + im.oM64) + grp.p0;
+      const int np = grp.np;
+      const int64_t pb = grp.prep_blocks, tiles = grp.tiles;
+      PP_REQUIRE(pb < (int64_t(1) << 31) && tiles < (int64_t(1) << 31), "wave too large");
+      P->steps.push_back([ctx, mf, np, pb](cudaStream_t st) {
+        mp64_prep_kernel<<<static_cast<unsigned>(pb), 256, 0, st>>>(mf, np);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(6);
+      P->step_work.push_back(0.0);
+      P->steps.push_back([ctx, mf, np, tiles](cudaStream_t st) {
+        mp64_fold_kernel<<<static_cast<unsigned>(tiles), kMp64Threads, kMp64Smem, st>>>(mf, np);
+        check_launch(ctx);
+      });
+      P->step_kind.push_back(18);
+      P->step_work.push_back(grp.cells);
+      launches += 2;
     }
     for (const auto &grp : wr.mg) { // large fixed-point folds of this wave, per launch group: prep -> stream-K fold
       const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + grp.p0;

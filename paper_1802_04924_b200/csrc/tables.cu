@@ -202,6 +202,16 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// FP64 synthetic tables that the fixed-point certificate rejects: (k + u) / 64,
+// k = splitmix % 641, u a 53-bit fraction (measured-cost-like values)
+__global__ void synth64_kernel(double *out, int64_t n, uint64_t seed, uint64_t stream) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t x = splitmix64(seed ^ stream ^ static_cast<uint64_t>(k) * 0x9E3779B97F4A7C15ULL);
+    out[k] = (static_cast<double>(x % 641) + static_cast<double>(x >> 11) * 0x1p-53) / 64.0;
+  }
+}
+
 __global__ void synth_kernel(int32_t *out, int64_t n, uint64_t seed, uint64_t stream) {
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -617,6 +627,36 @@ pp_status pp_tables_synthetic(pp_context *ctx, const pp_graph *gh, int32_t C, ui
     check_launch(ctx);
     if (t.xcells) {
       synth_kernel<<<grid, 256, 0, ctx->stream>>>(t.xfer32.p, t.xcells, seed, 0x58464552ULL << 32);
+      check_launch(ctx);
+    }
+    t.build_ms = ctx->end_ms();
+    *out = tp.release();
+  });
+}
+
+pp_status pp_tables_synthetic64(pp_context *ctx, const pp_graph *gh, int32_t C, uint64_t seed, pp_tables **out) {
+  return guard([&] {
+    PP_REQUIRE(ctx && gh && out, "pp_tables_synthetic64: null argument");
+    PP_REQUIRE(C >= 1 && C <= 65535, "configs must be in 1..65535");
+    const Graph &g = gh->impl;
+    auto tp = std::make_unique<pp_tables>();
+    Tables &t = tp->impl;
+    t.ctx = ctx;
+    init_layout(t, g, std::vector<int32_t>(static_cast<size_t>(g.nl), C));
+    t.configs.resize(static_cast<size_t>(4 * t.ncells));
+    for (int64_t k = 0; k < t.ncells; ++k) {
+      t.configs[static_cast<size_t>(4 * k)] = 1, t.configs[static_cast<size_t>(4 * k + 1)] = 1;
+      t.configs[static_cast<size_t>(4 * k + 2)] = 1, t.configs[static_cast<size_t>(4 * k + 3)] = k % C + 1;
+    }
+    t.mode = kFP64;
+    t.node.alloc(static_cast<size_t>(t.ncells));
+    t.xfer64.alloc(static_cast<size_t>(t.xcells));
+    ctx->begin();
+    const int grid = ctx->sms * 8;
+    synth64_kernel<<<grid, 256, 0, ctx->stream>>>(t.node.p, t.ncells, seed, 0x4e4f4445ULL << 32);
+    check_launch(ctx);
+    if (t.xcells) {
+      synth64_kernel<<<grid, 256, 0, ctx->stream>>>(t.xfer64.p, t.xcells, seed, 0x58464552ULL << 32);
       check_launch(ctx);
     }
     t.build_ms = ctx->end_ms();

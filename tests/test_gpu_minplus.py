@@ -102,3 +102,40 @@ def test_optimistic_cap_overflow_reruns_exactly(gpu, policy):
         pp.launch()
         c = pp.fetch()
         assert list(c.indices) == list(b.indices) and c.cost == b.cost
+
+
+# ---- FP64 large-table fold (minplus64.cuh) -------------------------------------------
+
+
+def test_fp64_large_fold_matches_generic(gpu):
+    """Non-dyadic (uncertified) FP64 tables: the 64x64-tile FP64 fold vs the
+    generic tiled fold — same IEEE sums in the reference's order, same argmins."""
+    import paper_1802_04924_b200 as P
+
+    g = P.series_parallel_graph(3, 40, 0.4)
+    ctx = P.Context(0)
+    t = P.synthetic_cost_tables64(g, 600, seed=9, ctx=ctx)
+    prof = P.PreparedPlan(g, tables=t, ctx=ctx).profile()
+    assert "mp64_fold" in [k for k, _, _ in prof]
+    a = P.plan_with_tables(g, t)
+    assert a.precision == "fp64"
+    ctx.set_kernel_policy("generic")
+    b = P.plan_with_tables(g, t)
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
+
+
+def test_fp64_large_fold_matches_fixed_point_on_dyadic_tables(gpu):
+    """The same dyadic tables planned in FP64 (precision forced) through the
+    FP64 large fold and in exact int32 through the U16 kernels: identical plans
+    (every FP64 sum of k/64 values is exact here)."""
+    import paper_1802_04924_b200 as P
+
+    g, t32 = P.synthetic_instance(4, 60, 520, 0.4, ctx=gpu.ctx)
+    cat, node, _, _, xfer = t32.download()
+    c64 = P.Context(0)
+    c64.set_precision("fp64")
+    t64 = P.upload_cost_tables(g, cat, node, xfer, c64)
+    assert "mp64_fold" in [k for k, _, _ in P.PreparedPlan(g, tables=t64, ctx=c64).profile()]
+    a, b = P.plan_with_tables(g, t32), P.plan_with_tables(g, t64)
+    assert a.precision == "fixed" and b.precision == "fp64"
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
