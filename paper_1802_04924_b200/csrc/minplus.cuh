@@ -112,6 +112,7 @@ struct MpFold {
   int64_t colmin_begin; // first mp_minima column block (blocks only for an original t2)
   int64_t rowmin_begin; // first mp_minima row block, counted after all column blocks (original t1)
   int64_t unit_begin;   // first stream-K unit (tile-major, chunk fastest)
+  int64_t tile_begin;   // first tile (data-parallel mode)
 };
 
 constexpr int kMpPrepBatch = 8; // chunks per mp_prep block when the minima are ready
@@ -442,8 +443,11 @@ __device__ __forceinline__ int64_t mp_first(int64_t b, int64_t units, int64_t G)
 // the CTA owning unit u: the largest b with b * units / G <= u
 __device__ __forceinline__ int64_t mp_owner(int64_t u, int64_t units, int64_t G) { return ((u + 1) * G - 1) / units; }
 
+// dp_tiles > 0: data-parallel mode for wide launches — CTA b takes whole tiles
+// b, b + G, ... (tile_begin order), so co-running CTAs share operand blocks in
+// L2 and no tile is split; 0: stream-K over the contiguous unit ranges.
 template <int JB>
-__global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *folds, int n, int64_t units) {
+__global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *folds, int n, int64_t units, int64_t dp_tiles) {
   extern __shared__ __align__(128) unsigned char mp_smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(mp_smem + kMpStages * kMpStageBytes);
   uint64_t *empty = full + kMpStages;
@@ -464,17 +468,8 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
 
   if (warp == kMpConsumers / 32) { // producer: one thread streams the CTA's units in order
     if (lane == 0) {
-      int64_t seg_hi = -1;
-      const MpFold *f = nullptr;
       int64_t nn = 0;
-      for (int64_t u = u_begin; u < u_end; ++u, ++nn) {
-        if (u >= seg_hi) {
-          const int fi = find_desc(folds, n, u, [](const MpFold &x) { return x.unit_begin; });
-          f = &folds[fi];
-          seg_hi = fi + 1 < n ? folds[fi + 1].unit_begin : units;
-        }
-        const int64_t local = u - f->unit_begin;
-        const int tile = static_cast<int>(local / f->nchunks), c = static_cast<int>(local % f->nchunks);
+      auto stage = [&](const MpFold *f, int tile, int c) {
         const int ti = tile / f->tiles_k, tk = tile % f->tiles_k;
         const int s = static_cast<int>(nn % kMpStages);
         const unsigned ph = static_cast<unsigned>(nn / kMpStages) & 1u;
@@ -484,6 +479,25 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
         bulk_g2s(st, f->A + (static_cast<int64_t>(ti) * f->nchunks + c) * (kMpChunk * kMpTile), kMpStageA, &full[s]);
         bulk_g2s(st + kMpStageA, f->B + (static_cast<int64_t>(tk) * f->nchunks + c) * (kMpChunk * kMpTile), kMpStageB,
                  &full[s]);
+        ++nn;
+      };
+      if (dp_tiles > 0) {
+        for (int64_t tg = blockIdx.x; tg < dp_tiles; tg += G) {
+          const MpFold *f = &folds[find_desc(folds, n, tg, [](const MpFold &x) { return x.tile_begin; })];
+          for (int c = 0; c < f->nchunks; ++c) stage(f, static_cast<int>(tg - f->tile_begin), c);
+        }
+      } else {
+        int64_t seg_hi = -1;
+        const MpFold *f = nullptr;
+        for (int64_t u = u_begin; u < u_end; ++u) {
+          if (u >= seg_hi) {
+            const int fi = find_desc(folds, n, u, [](const MpFold &x) { return x.unit_begin; });
+            f = &folds[fi];
+            seg_hi = fi + 1 < n ? folds[fi + 1].unit_begin : units;
+          }
+          const int64_t local = u - f->unit_begin;
+          stage(f, static_cast<int>(local / f->nchunks), static_cast<int>(local % f->nchunks));
+        }
       }
     }
     return;
@@ -495,15 +509,29 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
   constexpr int GL = (1 << JB) < kMpChunk ? (1 << JB) : kMpChunk; // j of a group inside one stage
   constexpr int GPS = kMpChunk / GL, CPG = (1 << JB) / GL;
   constexpr uint32_t LOW2 = ((1u << JB) - 1) * 0x10001u;
-  int64_t u = u_begin, nn = 0;
-  while (u < u_end) {
-    const int fi = find_desc(folds, n, u, [](const MpFold &x) { return x.unit_begin; });
+  int64_t u = u_begin, nn = 0, tg = blockIdx.x;
+  while (dp_tiles > 0 ? tg < dp_tiles : u < u_end) {
+    int fi, tile, c_first;
+    int64_t tile_lo, tile_hi, seg_lo, seg_end;
+    if (dp_tiles > 0) { // a whole tile
+      fi = find_desc(folds, n, tg, [](const MpFold &x) { return x.tile_begin; });
+      tile = static_cast<int>(tg - folds[fi].tile_begin);
+      c_first = 0;
+      tile_lo = seg_lo = folds[fi].unit_begin + static_cast<int64_t>(tile) * folds[fi].nchunks;
+      tile_hi = seg_end = tile_lo + folds[fi].nchunks;
+      tg += G;
+      u = seg_lo;
+    } else {
+      fi = find_desc(folds, n, u, [](const MpFold &x) { return x.unit_begin; });
+      const int64_t local = u - folds[fi].unit_begin;
+      tile = static_cast<int>(local / folds[fi].nchunks);
+      c_first = static_cast<int>(local % folds[fi].nchunks);
+      tile_lo = folds[fi].unit_begin + static_cast<int64_t>(tile) * folds[fi].nchunks;
+      tile_hi = tile_lo + folds[fi].nchunks;
+      seg_lo = u;
+      seg_end = min(u_end, tile_hi);
+    }
     const MpFold &f = folds[fi];
-    const int64_t local = u - f.unit_begin;
-    const int tile = static_cast<int>(local / f.nchunks);
-    const int c_first = static_cast<int>(local % f.nchunks);
-    const int64_t tile_lo = f.unit_begin + static_cast<int64_t>(tile) * f.nchunks, tile_hi = tile_lo + f.nchunks;
-    const int64_t seg_lo = u, seg_end = min(u_end, tile_hi);
 
     // key = value << (16 + JB) | j (group << JB | j-low): lowest value, then lowest j.
     // A group cut by a segment boundary contributes its part; parts combine by min.

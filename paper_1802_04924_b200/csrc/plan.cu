@@ -568,7 +568,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     struct MpGroup {
       size_t p0 = 0; // large folds [p0, p0 + np) in mpf, one prep + fold launch pair
       int np = 0;
-      int64_t units = 0, prep_blocks = 0; // stream-K units, mp_prep blocks
+      int64_t units = 0, prep_blocks = 0, tiles = 0; // stream-K units, mp_prep blocks, tiles
       int jb = 5;
       double cells = 0.0;
     };
@@ -930,6 +930,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             if (op.e1 < t.ne) rowmin_blocks += (f.nu + 7) / 8;
             f.unit_begin = G.units;
             G.units += static_cast<int64_t>(f.tiles_i) * f.tiles_k * f.nchunks;
+            f.tile_begin = G.tiles;
+            G.tiles += static_cast<int64_t>(f.tiles_i) * f.tiles_k;
             G.cells += static_cast<double>(f.nu) * f.nw * f.nv;
             mpf.push_back(f);
             ++G.np;
@@ -1510,6 +1512,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       const MpFold *mf = reinterpret_cast<const MpFold *>(dimg + im.oMP) + grp.p0;
       const int np = grp.np;
       const int64_t pb = grp.prep_blocks, units = grp.units;
+      // wide launches: whole tiles round-robin (no split tiles, operand blocks shared in L2)
+      const int64_t dp = grp.tiles >= 4 * int64_t(ctx->sms) ? grp.tiles : 0;
       PP_REQUIRE(pb < (int64_t(1) << 31), "wave too large");
       const unsigned G = static_cast<unsigned>(std::min<int64_t>(units, int64_t(ctx->sms)));
       const int jb = grp.jb;
@@ -1531,7 +1535,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       });
       P->step_kind.push_back(6);
       P->step_work.push_back(0.0);
-      P->steps.push_back([ctx, mf, np, units, G, jb](cudaStream_t st) {
+      P->steps.push_back([ctx, mf, np, units, G, jb, dp](cudaStream_t st) {
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1547,7 +1551,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
                                    : jb == 5 ? mp_fold_kernel<5>
                                    : jb == 4 ? mp_fold_kernel<4>
                                              : mp_fold_kernel<3>,
-                                   mf, np, units));
+                                   mf, np, units, dp));
         check_launch(ctx);
       });
       P->step_kind.push_back(8);
