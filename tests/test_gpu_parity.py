@@ -236,7 +236,11 @@ def test_evaluate_batch_matches_oracle(gpu, source):
 # plan — the hand-rolled barrier vs grid.sync(), dynamic vs static build chunks,
 # chain segments and merge absorption off, the early table build off
 KNOBS = [{"PARPLAN_GRID_BARRIER": "0"}, {"PARPLAN_BUILD_DYNAMIC": "0"}, {"PARPLAN_CHAINS": "0"},
-         {"PARPLAN_MERGE_FUSE": "0"}, {"PARPLAN_EARLY_BUILD": "0"}, {"PARPLAN_STAGE": "0", "PARPLAN_PANEL": "0"}]
+         {"PARPLAN_MERGE_FUSE": "0"}, {"PARPLAN_EARLY_BUILD": "0"}, {"PARPLAN_STAGE": "0", "PARPLAN_PANEL": "0"},
+         # narrow waves on the first thread-block cluster (cluster barriers between
+         # consecutive narrow waves; the staging-visibility rule of plan.cu's `seen`)
+         {"PARPLAN_NARROW_ITEMS": "64", "PARPLAN_CLUSTER": "1"}, {"PARPLAN_NARROW_ITEMS": "64", "PARPLAN_CLUSTER": "2"},
+         {"PARPLAN_NARROW_ITEMS": "256", "PARPLAN_CLUSTER": "4"}, {"PARPLAN_NARROW_ITEMS": "64", "PARPLAN_CHAINS": "0"}]
 
 
 @pytest.mark.parametrize("knobs", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()))
