@@ -31,6 +31,7 @@ const Nccl &nccl() {
     n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
     n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
     n.AllGather = reinterpret_cast<decltype(n.AllGather)>(sym("ncclAllGather"));
+    n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(sym("ncclBroadcast"));
     n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
     n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(sym("ncclGroupEnd"));
     n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
@@ -89,6 +90,10 @@ void comm_destroy(pp_context *ctx) {
 
 void all_gather(pp_context *ctx, const void *send, void *recv, size_t bytes, cudaStream_t st) {
   PP_NCCL(nccl().AllGather(send, recv, bytes, ncclUint8, static_cast<ncclComm_t>(ctx->comm), st));
+}
+
+void broadcast(pp_context *ctx, void *buf, size_t bytes, int root, cudaStream_t st) {
+  PP_NCCL(nccl().Broadcast(buf, buf, bytes, ncclUint8, root, static_cast<ncclComm_t>(ctx->comm), st));
 }
 
 void group_start() { PP_NCCL(nccl().GroupStart()); }

@@ -113,8 +113,9 @@ struct pp_prepared {
   size_t image_off = 0, image_bytes = 0, res_off = 0, res_bytes = 0, off_idx = 0, off_cost = 0, off_ovf = 0;
   bool mp_conservative = false; // min-plus folds with proven caps only (after an optimistic overflow)
   int k_bound = 8;
-  // row-sharded plans: image offset of the peer bases, rank count, the
-  // all-gather lists of the kind-15 steps (in order), IPC-opened peer bases
+  // row-sharded plans: image offset of the peer bases, rank count, the block
+  // lists of the collective steps (kind 15 all-gathers, kind 19 edge-range
+  // broadcasts; in order), IPC-opened peer bases
   size_t off_peer = SIZE_MAX;
   int nranks = 1;
   std::vector<std::vector<std::tuple<const void *, void *, size_t>>> gather_lists;
@@ -1398,7 +1399,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         for (const auto &x : part) all_gather(ctx, std::get<0>(x), std::get<1>(x), std::get<2>(x), st);
         group_end();
       });
-      P->gather_lists.push_back(part); // the k-th kind-15 step (virtual ranks copy these blocks themselves)
+      P->gather_lists.push_back(part); // the k-th collective step (virtual ranks copy these blocks themselves)
       P->step_kind.push_back(15);
       P->step_work.push_back(bytes);
     }
@@ -1416,13 +1417,54 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ba.node_blocks = static_cast<int32_t>(bp->node_blocks);
     ba.bw_uniform = bp->bw_uniform;
   }
-  if (bp && bp->grid > 0 && !use_fused) {
+  if (bp && bp->grid > 0 && !use_fused && !shard) {
     const BuildArgs a = ba;
     const int64_t grid = bp->grid;
     P->steps.push_back([ctx, a, grid](cudaStream_t st) { launch_build(ctx, st, a, grid); });
     P->step_kind.push_back(0);
     P->step_work.push_back(static_cast<double>(t.ncells + t.xcells));
     ++launches;
+  } else if (bp && bp->grid > 0 && !use_fused) {
+    // row-sharded plan: K1 sharded by edge — rank q builds the xfer tables of
+    // the edges whose blocks fall in its 1/NR of the edge blocks (whole edges),
+    // K2 (node costs, tiny) on every rank; then every rank's edge range is
+    // broadcast over NVLink (in place: the tables sit at offset 0 of every
+    // rank's plan memory)
+    const int64_t eblocks = bp->grid - bp->node_blocks;
+    std::vector<int> first(static_cast<size_t>(NR) + 1, t.ne);
+    for (int q = 0, e = 0; q <= NR; ++q) {
+      const int64_t want = eblocks * q / NR;
+      while (e < t.ne && bp->E[static_cast<size_t>(e)].blk_begin < want) ++e;
+      first[static_cast<size_t>(q)] = q == NR ? t.ne : e;
+    }
+    auto eblk = [&](int e) { return e < t.ne ? bp->E[static_cast<size_t>(e)].blk_begin : eblocks; };
+    BuildArgs a = ba;
+    a.edge_block0 = eblk(first[static_cast<size_t>(RK)]);
+    const int64_t grid = bp->node_blocks + eblk(first[static_cast<size_t>(RK) + 1]) - a.edge_block0;
+    P->steps.push_back([ctx, a, grid](cudaStream_t st) { launch_build(ctx, st, a, grid); });
+    P->step_kind.push_back(0);
+    P->step_work.push_back(static_cast<double>(t.ncells + t.xcells) / NR);
+    ++launches;
+    std::vector<std::tuple<const void *, void *, size_t>> ranges;
+    double bytes = 0.0;
+    for (int q = 0; q < NR; ++q) {
+      const int64_t c0 = t.xoff[static_cast<size_t>(first[static_cast<size_t>(q)])];
+      const int64_t c1 = t.xoff[static_cast<size_t>(first[static_cast<size_t>(q) + 1])];
+      double *p = t.xfer64.p + c0;
+      ranges.emplace_back(p, p, static_cast<size_t>(c1 - c0) * 8);
+      bytes += static_cast<double>(c1 - c0) * 8;
+    }
+    P->steps.push_back([ctx, ranges](cudaStream_t st) {
+      PP_REQUIRE(ctx->comm, "row-sharded plan without a communicator (virtual ranks run through pp_vgroup)");
+      group_start();
+      for (int q = 0; q < static_cast<int>(ranges.size()); ++q)
+        if (std::get<2>(ranges[static_cast<size_t>(q)]))
+          broadcast(ctx, std::get<1>(ranges[static_cast<size_t>(q)]), std::get<2>(ranges[static_cast<size_t>(q)]), q, st);
+      group_end();
+    });
+    P->gather_lists.push_back(ranges); // kind 19: entry q = rank q's range (virtual ranks copy it)
+    P->step_kind.push_back(19);
+    P->step_work.push_back(bytes);
   }
   if (mp_pbytes) { // large folds: tile counters 0 at rest, row minima 0xFF.. before their producers
     unsigned char *pz = db + off_mpp + mp_part, *ovf = dimg + im.oOvf;
@@ -2120,7 +2162,7 @@ static void run_group(std::vector<pp_prepared *> &Ps) {
     for (int r = 0; r < n; ++r) {
       pp_prepared &P = *Ps[static_cast<size_t>(r)];
       size_t &i = pos[static_cast<size_t>(r)];
-      while (i < P.steps.size() && P.step_kind[i] != 15) P.steps[i++](P.ctx->stream);
+      while (i < P.steps.size() && P.step_kind[i] != 15 && P.step_kind[i] != 19) P.steps[i++](P.ctx->stream);
       PP_CUDA(cudaEventRecord(ev[static_cast<size_t>(r)], P.ctx->stream));
       at_gather += i < P.steps.size();
     }
@@ -2131,6 +2173,16 @@ static void run_group(std::vector<pp_prepared *> &Ps) {
       for (int q = 0; q < n; ++q)
         if (q != r) PP_CUDA(cudaStreamWaitEvent(P.ctx->stream, ev[static_cast<size_t>(q)], 0));
       const auto &mine = P.gather_lists[k];
+      if (P.step_kind[pos[static_cast<size_t>(r)]] == 19) { // edge-range broadcast: rank q's range from rank q
+        for (int q = 0; q < n; ++q) {
+          if (q == r || !std::get<2>(mine[static_cast<size_t>(q)])) continue;
+          const auto &theirs = Ps[static_cast<size_t>(q)]->gather_lists[k][static_cast<size_t>(q)];
+          PP_CUDA(cudaMemcpyAsync(std::get<1>(mine[static_cast<size_t>(q)]), std::get<0>(theirs), std::get<2>(theirs),
+                                  cudaMemcpyDeviceToDevice, P.ctx->stream));
+        }
+        ++pos[static_cast<size_t>(r)];
+        continue;
+      }
       for (size_t j = 0; j < mine.size(); ++j) {
         const size_t bytes = std::get<2>(mine[j]);
         unsigned char *recv = static_cast<unsigned char *>(std::get<1>(mine[j]));

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kBuildThreads, 8) build_tables_kernel(BuildArg
     if (gi < a.ncells) node_cost_cell(a, gi);
     return;
   }
-  const int64_t eb = b - a.node_blocks;
+  const int64_t eb = b - a.node_blocks + a.edge_block0;
   // edge of this block: binary search over the edges' first blocks, staged
   // in shared memory (independent loads instead of a chain of dependent ones)
   constexpr int kStaged = 2048;

@@ -73,6 +73,7 @@ struct BuildArgs {
   int32_t nl, ne, D;
   int32_t node_blocks;
   double bw_uniform; // > 0 when every off-diagonal bandwidth is this value
+  int64_t edge_block0; // first edge block of this launch (row-sharded plans build an edge range per rank)
 };
 
 struct BuildPlan {
