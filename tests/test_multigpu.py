@@ -122,3 +122,20 @@ def test_virtual_ranks_config5_match_single_gpu(gpu, n, C):
     if C == 256:
         gold = next(c for c in _gold()["synthetic"] if c["configs"] == 256)
         assert [int(x) for x in r.indices] == gold["indices"] and float(r.cost).hex() == gold["cost"]
+
+
+@pytest.mark.gpu
+def test_mgpu_plan_without_torch():
+    """bin/mgpu_plan: NCCL unique id handed to forked per-GPU processes through a
+    pipe (no torch.distributed, no MPI); the row-sharded I64 plan equals the
+    reference golden."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import json
+
+    exe = os.path.join(ROOT, "paper_1802_04924_b200", "bin", "mgpu_plan")
+    p = subprocess.run([exe, "2", "inception_chain", "64"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    rows = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    gold = next(c for c in _gold()["builtins"] if c["model"] == "inception_chain" and c["devices"] == 64)
+    assert rows and all(r["cost"] == gold["cost"] for r in rows)
