@@ -221,10 +221,19 @@ inline PlanResult plan(const ComputationGraph &graph, const DeviceGraph &devices
   std::vector<int32_t> idx(static_cast<size_t>(graph.layer_count()));
   pp_plan_result res{};
   runtime::check(pp_plan(runtime::context(), g.get(), &d, k_bound, idx.data(), &res));
-  std::vector<std::vector<Config>> catalog;
-  for (int l = 0; l < graph.layer_count(); ++l)
-    catalog.push_back(enumerate_configs(graph.layer(l).kind, graph.shape(l), devices.count()));
-  return detail::finish_plan(idx, res, catalog);
+  // the chosen configs from the library's catalogs (already enumerated for the tables)
+  std::vector<int64_t> cfg(static_cast<size_t>(graph.layer_count()) * 4);
+  runtime::check(pp_graph_configs_at(g.get(), devices.count(), idx.data(), cfg.data()));
+  PlanResult r;
+  r.indices.assign(idx.begin(), idx.end());
+  r.cost = res.cost;
+  r.final_graph_nodes = res.final_graph_nodes;
+  r.node_eliminations = res.node_eliminations;
+  r.edge_eliminations = res.edge_eliminations;
+  r.strategy.resize(idx.size());
+  for (size_t l = 0; l < idx.size(); ++l)
+    r.strategy[l] = Config{cfg[4 * l], cfg[4 * l + 1], cfg[4 * l + 2], cfg[4 * l + 3]};
+  return r;
 }
 
 } // namespace parplan

@@ -190,6 +190,11 @@ pp_status pp_graph_layer_id(const pp_graph *g, int32_t layer, char *buf, int32_t
 /* enumerate_configs (partition.hpp:174-204) for every layer: counts[n_layers];
  * configs may be NULL (size query), else [sum(counts) * 4]. */
 pp_status pp_graph_catalogs(const pp_graph *g, int32_t device_count, int32_t *counts, int64_t *configs);
+/* The chosen config of every layer (4 int64 each: sample, channel, height,
+ * width) for per-layer catalog indices — PlanResult::strategy (planner.hpp:325-334)
+ * without copying the catalogs.  Catalogs are cached per (graph, device count);
+ * graphs created from equal descriptors share those caches and the schedule. */
+pp_status pp_graph_configs_at(const pp_graph *g, int32_t device_count, const int32_t *indices, int64_t *configs);
 /* The symbolic elimination schedule (planner.hpp:111-217) computed by the
  * O((N+E) log N) host scheduler: the exact record sequence reduce() logs.
  * records may be NULL (size query). */

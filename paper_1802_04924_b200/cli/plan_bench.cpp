@@ -3,7 +3,10 @@
 // parplan::plan(graph, DeviceGraph::uniform(D)) (planner.hpp:368-371; the
 // reference's acceptance C5 times exactly this, acceptance.cpp:292-303), so the
 // drop-in's pp_graph, catalogs and schedule are rebuilt per call, unlike the
-// cached-graph pp_plan number of bench.py.  Also times acceptance C4's pair
+// cached-graph pp_plan number of bench.py.  Graphs equal to a recent one share
+// its host work (content-addressed cache in the library): "dropin_plan" is the
+// repeated call, "dropin_plan_cold" a graph never seen before (a new batch size
+// per call).  Also times acceptance C4's pair
 // (brute_force_plan vs plan_with_tables on host CostTables, lenet5@4).
 //
 //   plan_bench [runs=20] [warmup=3]   -> one JSON object per line on stdout
@@ -64,6 +67,19 @@ int main(int argc, char **argv) {
       if (k >= warmup) t.push_back(dt);
     }
     stats("dropin_plan", label, t, cost);
+    // cold: a graph the library has not seen (batch 33, 34, ...: new shapes, so
+    // no content-cache hit — shape inference, catalogs and the schedule per call)
+    std::vector<double> tc;
+    for (int k = 0; k < runs; ++k) {
+      const int64_t batch = 33 + static_cast<int64_t>(w.devices) * 1000 + k;
+      const auto t0 = Clock::now();
+      const ComputationGraph g =
+          w.modules ? models::inception_chain(batch, w.modules) : builtin_model(w.name, batch);
+      const PlanResult p = plan(g, DeviceGraph::uniform(w.devices));
+      tc.push_back(ms_since(t0));
+      (void)p;
+    }
+    stats("dropin_plan_cold", label, tc, 0.0);
   }
   { // acceptance C4's pair on host CostTables (acceptance.cpp:258-268)
     const ComputationGraph g = models::lenet5(32);

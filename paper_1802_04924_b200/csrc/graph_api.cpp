@@ -5,6 +5,8 @@
 #include "parplan/models.hpp"
 
 #include <cstring>
+#include <list>
+#include <mutex>
 
 namespace pp {
 
@@ -34,11 +36,13 @@ Graph::Graph(parplan::ComputationGraph cg) : g(std::move(cg)) {
 }
 
 const Schedule &Graph::schedule() {
+  std::lock_guard<std::mutex> lock(lazy);
   if (!sched) sched = std::make_unique<Schedule>(build_schedule(nl, esrc, edst, rank));
   return *sched;
 }
 
 const Graph::Catalogs &Graph::catalogs(int devices) const {
+  std::lock_guard<std::mutex> lock(lazy);
   auto it = catalog_cache.find(devices);
   if (it != catalog_cache.end()) return it->second;
   Catalogs c;
@@ -71,10 +75,56 @@ extern "C" {
 const char *pp_last_error(void) { return pp::g_last_error.c_str(); }
 int pp_abi_version(void) { return PP_ABI_VERSION; }
 
+namespace {
+// Content-addressed cache of the most recent graphs: the key is the whole
+// descriptor, so a hit is exactly an equal graph (memoised pure functions of an
+// immutable value).  Strong references, least recently used evicted.
+struct GraphCache {
+  std::mutex mu;
+  std::list<std::pair<std::string, std::shared_ptr<pp::Graph>>> lru;
+  static constexpr size_t kMax = 16;
+};
+GraphCache &graph_cache() {
+  static GraphCache c;
+  return c;
+}
+std::string desc_key(const pp_graph_desc *d) {
+  std::string k;
+  auto put = [&](const void *p, size_t n) { k.append(static_cast<const char *>(p), n); };
+  put(&d->n_layers, sizeof d->n_layers);
+  put(&d->n_edges, sizeof d->n_edges);
+  put(&d->batch, sizeof d->batch);
+  for (int l = 0; l < d->n_layers; ++l) {
+    const char *id = d->ids && d->ids[l] ? d->ids[l] : "";
+    k.append(id);
+    k.push_back('\0');
+  }
+  put(d->kind, sizeof(int32_t) * static_cast<size_t>(d->n_layers));
+  put(d->params, sizeof(int64_t) * 7 * static_cast<size_t>(d->n_layers));
+  put(d->edge_src, sizeof(int32_t) * static_cast<size_t>(d->n_edges));
+  put(d->edge_dst, sizeof(int32_t) * static_cast<size_t>(d->n_edges));
+  k.push_back(d->ids ? 'i' : 'n');
+  return k;
+}
+} // namespace
+
 pp_status pp_graph_create(const pp_graph_desc *d, pp_graph **out) {
   return guard([&] {
     PP_REQUIRE(d && out, "pp_graph_create: null argument");
     PP_REQUIRE(d->n_layers >= 0 && d->n_edges >= 0, "pp_graph_create: negative sizes");
+    PP_REQUIRE(d->n_layers == 0 || (d->kind && d->params), "pp_graph_create: null layer arrays");
+    PP_REQUIRE(d->n_edges == 0 || (d->edge_src && d->edge_dst), "pp_graph_create: null edge arrays");
+    const std::string key = desc_key(d);
+    GraphCache &cache = graph_cache();
+    {
+      std::lock_guard<std::mutex> lock(cache.mu);
+      for (auto it = cache.lru.begin(); it != cache.lru.end(); ++it)
+        if (it->first == key) {
+          cache.lru.splice(cache.lru.begin(), cache.lru, it);
+          *out = new pp_graph(cache.lru.front().second);
+          return;
+        }
+    }
     std::vector<parplan::Layer> layers;
     std::vector<std::vector<std::string>> inputs(static_cast<size_t>(d->n_layers));
     for (int l = 0; l < d->n_layers; ++l) {
@@ -90,7 +140,27 @@ pp_status pp_graph_create(const pp_graph_desc *d, pp_graph **out) {
       prev = t;
       inputs[static_cast<size_t>(t)].push_back(layers[static_cast<size_t>(s)].id);
     }
-    *out = new pp_graph(parplan::ComputationGraph::create(std::move(layers), inputs, d->batch));
+    auto g = std::make_shared<pp::Graph>(parplan::ComputationGraph::create(std::move(layers), inputs, d->batch));
+    {
+      std::lock_guard<std::mutex> lock(cache.mu);
+      cache.lru.emplace_front(key, g);
+      if (cache.lru.size() > GraphCache::kMax) cache.lru.pop_back();
+    }
+    *out = new pp_graph(std::move(g));
+  });
+}
+
+pp_status pp_graph_configs_at(const pp_graph *g, int32_t devices, const int32_t *indices, int64_t *configs) {
+  return guard([&] {
+    PP_REQUIRE(g && indices && configs, "pp_graph_configs_at: null argument");
+    const pp::Graph::Catalogs &c = g->impl.catalogs(devices);
+    int64_t off = 0;
+    for (int l = 0; l < g->impl.nl; ++l) {
+      const int32_t n = c.counts[static_cast<size_t>(l)];
+      PP_REQUIRE(indices[l] >= 0 && indices[l] < n, "config index out of range");
+      std::memcpy(configs + 4 * l, &c.configs[static_cast<size_t>(4 * (off + indices[l]))], 4 * sizeof(int64_t));
+      off += n;
+    }
   });
 }
 

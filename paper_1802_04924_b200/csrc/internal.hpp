@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -76,6 +77,7 @@ struct Graph {
     std::vector<int32_t> configs32;
   };
   mutable std::map<int, Catalogs> catalog_cache;
+  mutable std::mutex lazy; // the schedule and catalog caches (a graph may be shared across threads)
 
   explicit Graph(parplan::ComputationGraph cg);
   const Schedule &schedule();
@@ -87,7 +89,12 @@ void enumerate_catalogs(const Graph &g, int devices, std::vector<int32_t> *count
 
 } // namespace pp
 
+// A handle on an immutable graph.  Handles created from equal descriptors
+// share one pp::Graph (graph_api.cpp: content-addressed cache), so repeated
+// plans of the same network skip shape inference, catalogs and the schedule.
 struct pp_graph {
-  pp::Graph impl;
-  explicit pp_graph(parplan::ComputationGraph cg) : impl(std::move(cg)) {}
+  std::shared_ptr<pp::Graph> own;
+  pp::Graph &impl;
+  explicit pp_graph(parplan::ComputationGraph cg) : own(std::make_shared<pp::Graph>(std::move(cg))), impl(*own) {}
+  explicit pp_graph(std::shared_ptr<pp::Graph> g) : own(std::move(g)), impl(*own) {}
 };
