@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "minplus.cuh"
 #include "minplus64.cuh"
+#include "mp_plan.hpp"
 
 #include <array>
 #include <algorithm>
@@ -328,214 +329,43 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       }
   // rows of a fold's t1 / a merge's operands this rank works on
   auto nu_eff = [&](int id) { return shard ? lrows(id) : rows[static_cast<size_t>(id)]; };
-  // ---- large fixed-point folds: span certificate + per-wave scratch -----------
-  // Span bounds per table (rows: max over rows of max-min; cols likewise),
-  // propagated through the log: fold R(out) <= R(t2), K(out) <= K(t1);
-  // merge R = R1 + R2, K = K1 + K2.  A fold takes the U16x2 kernel when
-  // rowspan(w + t1) + colspan(t2) leaves room for JB >= 3 argmin bits
-  // (minplus.cuh); a wave's folds share the smallest JB among them.
-  std::vector<char> large(s.ops.size(), 0);
-  std::vector<int> fold_jb(s.ops.size(), 0);
-  struct MpLayout {
-    size_t ra, cb, A, B, cnt; // A, B: per-wave section; cnt, ra, cb: persistent section
-    int nchunks, tiles_i, tiles_k;
-  };
-  std::vector<MpLayout> mpl(s.ops.size());
-  std::vector<std::vector<int>> wave_group_jb(static_cast<size_t>(s.n_waves) + 1); // JB per launch group
-  std::vector<int> mp_group(s.ops.size(), 0);
-  std::vector<int64_t> fold_m(s.ops.size(), 0);                    // bound on a fold's minima (cap - 1)
-  std::vector<char> fold_opt(s.ops.size(), 0);                     // optimistic cap (checked on the device)
-  // proven caps only: after an optimistic run overflowed, on request, or
-  // row-sharded (every rank must take the same path)
-  const bool conservative = P->mp_conservative || ctx->mp_conservative || shard;
-  std::vector<int> mp_consumer(static_cast<size_t>(E_total), -1);  // large fold reading a table as t1
-  std::vector<int> mp_consumer2(static_cast<size_t>(E_total), -1); // large fold reading a table as t2
-  std::vector<int> mp_producer(static_cast<size_t>(E_total), -1); // large fold writing a table
-  std::vector<char> mp_merge_out(static_cast<size_t>(E_total), 0); // table written by an mp_merge
-  // persistent section: stream-K partial slots | counters (0 at rest) | ra, cb (0xFF.. before use)
-  size_t mp_bytes = 0, mp_part = 0, mp_cnt = 0, mp_ra = 0, mp_cb = 0, mp_chainb = 0;
-  struct MpRun {
-    int w0 = 0;
-    std::vector<int> ops;
-    int R = 1;
-  };
-  std::vector<MpRun> mp_runs;
-  std::vector<int> mp_run_of(s.ops.size(), -1);
-  if constexpr (std::is_same_v<T, int32_t>) {
-    std::vector<int64_t> R(static_cast<size_t>(E_total), 0), Kc(static_cast<size_t>(E_total), 0);
-    for (int e = 0; e < t.ne; ++e) {
-      R[static_cast<size_t>(e)] = t.row_span[static_cast<size_t>(e)];
-      Kc[static_cast<size_t>(e)] = t.col_span[static_cast<size_t>(e)];
-    }
-    for (size_t oi = 0; oi < s.ops.size(); ++oi) {
-      const Op &op = s.ops[oi];
-      const size_t a = static_cast<size_t>(op.e1), b2 = static_cast<size_t>(op.e2), o = static_cast<size_t>(op.ne);
-      if (op.type) {
-        R[o] = R[a] + R[b2];
-        Kc[o] = Kc[a] + Kc[b2];
-        continue;
-      }
-      R[o] = R[b2];
-      Kc[o] = Kc[a];
-      const int nu = rows[a], nw = t.counts[static_cast<size_t>(op.removed)], nv = cols[b2];
-      // every minimum <= min(rowspan(w + t1), colspan(t2)) (minplus.cuh: cap)
-      fold_m[oi] = std::min(t.node_span[static_cast<size_t>(op.removed)] + R[a], Kc[b2]);
-      fold_jb[oi] = fold_m[oi] < 32768 ? mp_jbits(fold_m[oi]) : 0;
-      // optimistic JB 6 (cap 511, checked in the epilogue) unless conservative
-      if (!conservative) fold_opt[oi] = 1, fold_jb[oi] = kMpOptJB;
-      large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && fold_jb[oi] > 0 && !ctx->no_minplus;
-      if (large[oi] && nu_eff(op.e1) > 0) {
-        mp_consumer[a] = static_cast<int>(oi);
-        mp_consumer2[b2] = static_cast<int>(oi);
-        mp_producer[o] = static_cast<int>(oi);
-      }
-    }
-    for (const Op &op : s.ops) // merges feeding a large fold's t2 run as mp_merge (with its column minima)
-      if (op.type && !shard && mp_consumer2[static_cast<size_t>(op.ne)] >= 0) mp_merge_out[static_cast<size_t>(op.ne)] = 1;
-    auto take = [&](size_t &at, size_t bytes) {
-      const size_t o = at;
-      at += align256(bytes);
-      return o;
-    };
-    // chain runs (minplus.cuh: mp_chain): consecutive one-fold waves whose
-    // folds chain through t1 and whose t2 exist before the run
-    if (!shard && kn.mp_chain) {
-      MpRun cur;
-      auto close = [&] {
-        if (static_cast<int>(cur.ops.size()) >= kn.mp_chain_min) mp_runs.push_back(cur);
-        cur = MpRun{};
-      };
-      for (int w = 1; w <= s.n_waves; ++w) {
-        const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
-        const int oi = s.exec[static_cast<size_t>(x0)];
-        const Op &op = s.ops[static_cast<size_t>(oi)];
-        const bool ok = x1 - x0 == 1 && large[static_cast<size_t>(oi)] && !op.type &&
-                        cols[static_cast<size_t>(op.e2)] <= kMpChainCols &&
-                        t.counts[static_cast<size_t>(op.removed)] <= kMpChainNw &&
-                        rows[static_cast<size_t>(op.e1)] <= kMpChainRows * ctx->sms;
-        if (!ok) {
-          close();
-          continue;
-        }
-        const bool extends = !cur.ops.empty() && op.e1 == s.ops[static_cast<size_t>(cur.ops.back())].ne &&
-                             prod_wave[static_cast<size_t>(op.e2)] < cur.w0;
-        if (!extends) {
-          close();
-          cur.w0 = w;
-        }
-        cur.ops.push_back(oi);
-      }
-      close();
-      for (size_t r = 0; r < mp_runs.size(); ++r)
-        for (int oi : mp_runs[r].ops) {
-          mp_run_of[static_cast<size_t>(oi)] = static_cast<int>(r);
-          // the run computes its row minima itself and feeds no column minima:
-          // consumers of its outputs run their own minima passes
-          mp_producer[static_cast<size_t>(s.ops[static_cast<size_t>(oi)].ne)] = -1;
-        }
-      for (MpRun &run : mp_runs) {
-        run.R = (rows[static_cast<size_t>(s.ops[static_cast<size_t>(run.ops[0])].e1)] + ctx->sms - 1) / ctx->sms;
-        for (int oi : run.ops) {
-          const Op &op = s.ops[static_cast<size_t>(oi)];
-          MpLayout &L = mpl[static_cast<size_t>(oi)];
-          L.nchunks = (t.counts[static_cast<size_t>(op.removed)] + kMpChunk - 1) / kMpChunk;
-          L.tiles_i = L.tiles_k = 1;
-          L.B = take(mp_chainb, static_cast<size_t>(L.nchunks) * kMpChunk * kMpChainCols * 2);
-          L.cb = take(mp_cb, static_cast<size_t>(cols[static_cast<size_t>(op.e2)]) * 4);
-          L.ra = take(mp_ra, 4);
-        }
-      }
-    }
-    // per wave, in launch groups of at most kMpGroupBytes of operand blocks
-    // (a wide wave — 471 folds of config 5 — would need 45 GB at C = 4096):
-    // the operand blocks and tile counters (restored after every use) of one
-    // group are reused by the next group / wave
-    constexpr size_t kMpGroupBytes = size_t(2) << 30;
-    for (int w = 1; w <= s.n_waves; ++w) {
-      size_t off = 0, coff = 0;
-      int g = 0;
-      wave_group_jb[static_cast<size_t>(w)].assign(1, kMpOptJB);
-      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = s.exec[static_cast<size_t>(x)];
-        if (!large[static_cast<size_t>(oi)] || mp_run_of[static_cast<size_t>(oi)] >= 0) continue;
-        const Op &op = s.ops[static_cast<size_t>(oi)];
-        MpLayout &L = mpl[static_cast<size_t>(oi)];
-        const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)],
-                  nv = cols[static_cast<size_t>(op.e2)];
-        if (nu == 0) continue; // no rows of this fold on this rank
-        L.tiles_i = (nu + kMpTile - 1) / kMpTile;
-        L.tiles_k = (nv + kMpTile - 1) / kMpTile;
-        L.nchunks = (nw + kMpChunk - 1) / kMpChunk;
-        const size_t need = align256(static_cast<size_t>(L.tiles_i) * L.nchunks * kMpStageA) +
-                            align256(static_cast<size_t>(L.tiles_k) * L.nchunks * kMpStageB);
-        if (off > 0 && off + need > kMpGroupBytes) { // close the group
-          mp_bytes = std::max(mp_bytes, off);
-          mp_cnt = std::max(mp_cnt, coff);
-          off = coff = 0;
-          ++g;
-          wave_group_jb[static_cast<size_t>(w)].push_back(kMpOptJB);
-        }
-        mp_group[static_cast<size_t>(oi)] = g;
-        int &gjb = wave_group_jb[static_cast<size_t>(w)].back();
-        gjb = std::min(gjb, fold_jb[static_cast<size_t>(oi)]);
-        L.A = take(off, static_cast<size_t>(L.tiles_i) * L.nchunks * kMpStageA);
-        L.B = take(off, static_cast<size_t>(L.tiles_k) * L.nchunks * kMpStageB);
-        L.cnt = take(coff, static_cast<size_t>(L.tiles_i) * L.tiles_k * 4);
-        L.ra = take(mp_ra, static_cast<size_t>(nu) * 4);
-        L.cb = take(mp_cb, static_cast<size_t>(nv) * 4);
-      }
-      mp_bytes = std::max(mp_bytes, off);
-      mp_cnt = std::max(mp_cnt, coff);
-    }
-    if (!mp_runs.empty())
-      for (const MpRun &run : mp_runs) // per device, every prepare (cheap)
-        for (int jb : {4, 5, 6})
-          PP_CUDA(cudaFuncSetAttribute(mp_chain_launch(jb, run.R), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kMpChainSmem)));
-    if (mp_bytes) {
-      mp_part = static_cast<size_t>(ctx->sms) * kMpTileCells * 4;
-      // per device, every prepare (cheap; no process-wide cache across devices)
-      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
-      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
-      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
-      PP_CUDA(cudaFuncSetAttribute(mp_fold_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
-    }
-  }
-  // ---- large FP64 folds (minplus64.cuh): per wave, launch groups of operand blocks
-  std::vector<char> large64(s.ops.size(), 0);
-  std::vector<int> mp64_group(s.ops.size(), 0);
-  std::vector<std::array<size_t, 2>> mp64_off(s.ops.size(), {0, 0}); // A, B in the per-wave section
-  if constexpr (std::is_same_v<T, double>) {
-    constexpr size_t kGroupBytes = size_t(2) << 30;
-    for (int w = 1; w <= s.n_waves; ++w) {
-      size_t off = 0;
-      int g = 0;
-      for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
-        const int oi = s.exec[static_cast<size_t>(x)];
-        const Op &op = s.ops[static_cast<size_t>(oi)];
-        if (op.type || ctx->no_minplus) continue;
-        const int nu = nu_eff(op.e1), nw = t.counts[static_cast<size_t>(op.removed)], nv = cols[static_cast<size_t>(op.e2)];
-        // below ~512 rows / columns a wave holds too few 64x64 tiles: the generic kernels win
-        if (nu < kMp64MinSide || nv < kMp64MinSide || nw < kMp64Chunk * 2) continue;
-        large64[static_cast<size_t>(oi)] = 1;
-        const int nch = (nw + kMp64Chunk - 1) / kMp64Chunk;
-        const size_t a = align256(static_cast<size_t>((nu + kMp64Tile - 1) / kMp64Tile) * nch * kMp64StageA);
-        const size_t b = align256(static_cast<size_t>((nv + kMp64Tile - 1) / kMp64Tile) * nch * kMp64StageA);
-        if (off > 0 && off + a + b > kGroupBytes) {
-          mp_bytes = std::max(mp_bytes, off);
-          off = 0;
-          ++g;
-        }
-        mp64_group[static_cast<size_t>(oi)] = g;
-        mp64_off[static_cast<size_t>(oi)] = {off, off + a};
-        off += a + b;
-      }
-      mp_bytes = std::max(mp_bytes, off);
-    }
-    if (mp_bytes)
-      PP_CUDA(cudaFuncSetAttribute(mp64_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMp64Smem)));
-  }
-  const size_t mp_pbytes = mp_part + mp_cnt + mp_ra + mp_cb + mp_chainb;
+  // ---- large folds (U16 fixed point / FP64): certificate, chain runs, scratch layout
+  MinplusPlan mp;
+  mp.build<T>(MinplusPlan::In{s, t, rows, cols, nu_eff, shard, P->mp_conservative || ctx->mp_conservative || shard,
+                              ctx->no_minplus, ctx->sms, kn.mp_chain != 0, kn.mp_chain_min, prod_wave});
+  using MpLayout = MinplusPlan::Layout;
+  using MpRun = MinplusPlan::Run;
+  auto &large = mp.large;
+  auto &fold_jb = mp.fold_jb;
+  auto &fold_m = mp.fold_m;
+  auto &fold_opt = mp.fold_opt;
+  auto &mpl = mp.mpl;
+  auto &wave_group_jb = mp.wave_group_jb;
+  auto &mp_group = mp.mp_group;
+  auto &mp_consumer = mp.mp_consumer;
+  auto &mp_consumer2 = mp.mp_consumer2;
+  auto &mp_producer = mp.mp_producer;
+  auto &mp_merge_out = mp.mp_merge_out;
+  auto &mp_runs = mp.runs;
+  auto &mp_run_of = mp.run_of;
+  auto &large64 = mp.large64;
+  auto &mp64_group = mp.mp64_group;
+  auto &mp64_off = mp.mp64_off;
+  const size_t mp_bytes = mp.bytes, mp_part = mp.part, mp_cnt = mp.cnt, mp_ra = mp.ra, mp_cb = mp.cb,
+               mp_chainb = mp.chainb;
+  const size_t mp_pbytes = mp.pbytes();
+  (void)mp_consumer;
+  (void)mp_group;
+  // dynamic shared memory allowances: per device, so set on every prepare (cheap)
+  for (const MpRun &run : mp_runs)
+    for (int jb : {4, 5, 6})
+      PP_CUDA(cudaFuncSetAttribute(mp_chain_launch(jb, run.R), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kMpChainSmem)));
+  if (mp_part)
+    for (auto fn : {mp_fold_kernel<6>, mp_fold_kernel<5>, mp_fold_kernel<4>, mp_fold_kernel<3>})
+      PP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
+  if (mp_bytes && std::is_same_v<T, double>)
+    PP_CUDA(cudaFuncSetAttribute(mp64_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMp64Smem)));
 
   const size_t tables_bytes =
       bp ? align256(static_cast<size_t>(t.ncells) * 8) * 3 + align256(static_cast<size_t>(t.xcells) * 8) : 0;
