@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) mp_merge_kernel(const MpMerge *ms, int n)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-__global__ void __launch_bounds__(256) mp_prep_kernel(const MpFold *folds, int n) {
+__global__ void __launch_bounds__(256, 3) mp_prep_kernel(const MpFold *folds, int n) {
   pdl_launch_dependents(); // the fold may be scheduled now; it waits for this grid in griddepcontrol.wait
   const int64_t b = blockIdx.x;
   const MpFold &f = folds[find_desc(folds, n, b, [](const MpFold &x) { return x.prep_begin; })];
