@@ -173,6 +173,15 @@ pp_status pp_vgroup_create(int32_t device, int32_t nranks, pp_vgroup **out);
 pp_status pp_vgroup_plan(pp_vgroup *group, const pp_graph *g, const pp_device_desc *dev, pp_tables *t,
                          int32_t k_bound, int32_t *indices, pp_plan_result *res);
 pp_status pp_vgroup_destroy(pp_vgroup *group);
+/* Host-only (no GPU): the row-sharded layout a context with nranks ranks uses
+ * for this graph and per-layer config counts — for every table id of the
+ * elimination log (originals then derived): rows per rank block, this rank's
+ * first row and row count; and every all-gather as (wave, table id): derived t2
+ * before its fold's wave, then derived final edges at wave n_waves + 1.  Call
+ * with NULL arrays to get n_tables / n_gathers. */
+pp_status pp_shard_layout(const pp_graph *g, const int32_t *counts, int32_t nranks, int32_t rank, int32_t *n_tables,
+                          int32_t *blk, int32_t *first, int32_t *local_rows, int32_t *n_gathers, int32_t *gather_wave,
+                          int32_t *gather_table);
 /* kernel launches issued on this context since creation */
 pp_status pp_context_launch_count(const pp_context *ctx, int64_t *launches);
 

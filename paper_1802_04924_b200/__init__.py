@@ -17,6 +17,7 @@ from .capi import (  # noqa: F401
     PlanResult,
     PreparedPlan,
     VirtualRanks,
+    shard_layout,
     ReducedGraph,
     brute_force_plan,
     build_cost_tables,

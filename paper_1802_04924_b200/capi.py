@@ -91,6 +91,8 @@ _SIGS = {
     "pp_context_attach_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_char_p]),
     "pp_context_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "pp_vgroup_create": (C.c_int, [C.c_int32, C.c_int32, _pp]),
+    "pp_shard_layout": (C.c_int, [_vp, _i32p, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p]),
     "pp_vgroup_plan": (C.c_int, [_vp, _vp, C.c_void_p, _vp, C.c_int32, _i32p, C.POINTER(_PlanResult)]),
     "pp_vgroup_destroy": (C.c_int, [_vp]),
     "pp_graph_create": (C.c_int, [C.POINTER(_GraphDesc), _pp]),
@@ -568,6 +570,19 @@ def plan(graph: ComputationGraph, devices: DeviceGraph, k_bound: int = 8, ctx: O
     d = devices._desc()
     _check(lib().pp_plan(ctx.h, graph.h, C.byref(d), k_bound, idx, C.byref(r)))
     return _result(idx, r)
+
+
+def shard_layout(graph: "ComputationGraph", counts, nranks: int, rank: int):
+    """Host-only: the row-sharded layout (shard.hpp) -> (blk, first, local_rows)
+    per table id of the log, and the all-gathers as [(wave, table id)]."""
+    counts = np.ascontiguousarray(counts, np.int32)
+    nt, ng = C.c_int32(), C.c_int32()
+    _check(lib().pp_shard_layout(graph.h, counts, nranks, rank, C.byref(nt), None, None, None, C.byref(ng), None, None))
+    blk, first, local = (np.zeros(nt.value, np.int32) for _ in range(3))
+    gw, gt = np.zeros(max(ng.value, 1), np.int32), np.zeros(max(ng.value, 1), np.int32)
+    _check(lib().pp_shard_layout(graph.h, counts, nranks, rank, C.byref(nt), _ptr(blk), _ptr(first), _ptr(local),
+                                 C.byref(ng), _ptr(gw), _ptr(gt)))
+    return blk, first, local, list(zip(gw[:ng.value].tolist(), gt[:ng.value].tolist()))
 
 
 class VirtualRanks:

@@ -1,6 +1,7 @@
 // graph_api.cpp — host half of the C ABI: graphs, catalogs, the symbolic
 // schedule, error reporting.  No CUDA here; all of it works without a GPU.
 #include "internal.hpp"
+#include "shard.hpp"
 
 #include "parplan/models.hpp"
 
@@ -241,6 +242,30 @@ pp_status pp_graph_schedule(const pp_graph *g, int32_t *n, pp_record *recs, int3
         const pp::Op &o = s.ops[k];
         recs[k] = pp_record{o.type, o.removed, o.e1, o.e2, o.ne, o.u, o.v, o.wave};
       }
+  });
+}
+
+pp_status pp_shard_layout(const pp_graph *g, const int32_t *counts, int32_t nranks, int32_t rank, int32_t *n_tables,
+                          int32_t *blk, int32_t *first, int32_t *local_rows, int32_t *n_gathers, int32_t *gather_wave,
+                          int32_t *gather_table) {
+  return guard([&] {
+    PP_REQUIRE(g && counts && n_tables && n_gathers, "pp_shard_layout: null argument");
+    PP_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / world size");
+    const pp::Schedule &s = const_cast<pp_graph *>(g)->impl.schedule();
+    const int E = static_cast<int>(s.esrc.size());
+    *n_tables = E;
+    for (int id = 0; id < E; ++id) {
+      const int rows = counts[s.esrc[static_cast<size_t>(id)]];
+      if (blk) blk[id] = pp::shard_blk(rows, nranks);
+      if (first) first[id] = pp::shard_first(rows, nranks, rank);
+      if (local_rows) local_rows[id] = pp::shard_rows(rows, nranks, rank);
+    }
+    const auto gs = pp::shard_gathers(s, g->impl.ne);
+    *n_gathers = static_cast<int32_t>(gs.size());
+    for (size_t k = 0; k < gs.size(); ++k) {
+      if (gather_wave) gather_wave[k] = gs[k].first;
+      if (gather_table) gather_table[k] = gs[k].second;
+    }
   });
 }
 

@@ -15,6 +15,7 @@
 #include "minplus.cuh"
 #include "minplus64.cuh"
 #include "mp_plan.hpp"
+#include "shard.hpp"
 
 #include <array>
 #include <algorithm>
@@ -274,11 +275,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   // unwinds identically.
   const int NR = ctx->nranks > 1 ? ctx->nranks : 1, RK = NR > 1 ? ctx->rank : 0;
   const bool shard = NR > 1;
-  auto blk = [&](int id) { return (rows[static_cast<size_t>(id)] + NR - 1) / NR; };
-  auto lr0 = [&](int id) { return std::min(rows[static_cast<size_t>(id)], RK * blk(id)); };
-  auto lrows = [&](int id) {
-    return std::max(0, std::min(rows[static_cast<size_t>(id)], (RK + 1) * blk(id)) - lr0(id));
-  };
+  auto blk = [&](int id) { return shard_blk(rows[static_cast<size_t>(id)], NR); };
+  auto lr0 = [&](int id) { return shard_first(rows[static_cast<size_t>(id)], NR, RK); };
+  auto lrows = [&](int id) { return shard_rows(rows[static_cast<size_t>(id)], NR, RK); };
 
   // ---- memory plan ----------------------------------------------------------
   auto cells = [&](int id) { return static_cast<size_t>(rows[static_cast<size_t>(id)]) * cols[static_cast<size_t>(id)]; };
@@ -1023,6 +1022,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       ee.push_back(EnumEdge{t2p(id), pos[static_cast<size_t>(s.esrc[static_cast<size_t>(id)])],
                             pos[static_cast<size_t>(s.edst[static_cast<size_t>(id)])], cols[static_cast<size_t>(id)], 0});
     }
+    if (shard) { // the gathers issued above follow shard.hpp's schedule (pp_shard_layout, host-tested)
+      size_t n = im.final_gathers.size();
+      for (const auto &w : im.waves) n += w.gathers.size();
+      PP_REQUIRE(n == shard_gathers(s, t.ne).size(), "row-sharded plan: all-gather schedule mismatch");
+    }
     // row-sharded: argmin tables stay on their ranks; the unwind reads the
     // owner's row through the peer bases (no gather of the argmin tables)
     // unwind records (kernels.cuh finish_block), visited last wave first and
@@ -1261,12 +1265,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     // broadcast over NVLink (in place: the tables sit at offset 0 of every
     // rank's plan memory)
     const int64_t eblocks = bp->grid - bp->node_blocks;
-    std::vector<int> first(static_cast<size_t>(NR) + 1, t.ne);
-    for (int q = 0, e = 0; q <= NR; ++q) {
-      const int64_t want = eblocks * q / NR;
-      while (e < t.ne && bp->E[static_cast<size_t>(e)].blk_begin < want) ++e;
-      first[static_cast<size_t>(q)] = q == NR ? t.ne : e;
-    }
+    std::vector<int64_t> eb0(static_cast<size_t>(t.ne));
+    for (int e = 0; e < t.ne; ++e) eb0[static_cast<size_t>(e)] = bp->E[static_cast<size_t>(e)].blk_begin;
+    const std::vector<int> first = shard_edges(eb0, eblocks, NR);
     auto eblk = [&](int e) { return e < t.ne ? bp->E[static_cast<size_t>(e)].blk_begin : eblocks; };
     BuildArgs a = ba;
     a.edge_block0 = eblk(first[static_cast<size_t>(RK)]);

@@ -139,3 +139,58 @@ def test_mgpu_plan_without_torch():
     rows = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
     gold = next(c for c in _gold()["builtins"] if c["model"] == "inception_chain" and c["devices"] == 64)
     assert rows and all(r["cost"] == gold["cost"] for r in rows)
+
+
+# ---- the row-sharded layout, host only (shard.hpp via pp_shard_layout) -----------
+
+def _restated_layout(g, counts, nranks, rank):
+    """Python restatement of the row-block arithmetic and the all-gather schedule."""
+    import numpy as np
+
+    recs, n_waves = g.schedule()
+    es, ed, _ = g.edges()
+    src = list(es)
+    for rec in recs:  # derived edge ids are assigned in log order (planner.hpp:220-227)
+        assert rec[4] == len(src)
+        src.append(rec[5])
+    blk, first, local = [], [], []
+    for s in src:
+        rows = int(counts[s])
+        b = -(-rows // nranks)
+        f = min(rows, rank * b)
+        blk.append(b)
+        first.append(f)
+        local.append(max(0, min(rows, (rank + 1) * b) - f))
+    ne = g.n_edges
+    gathers = []
+    for w in range(1, n_waves + 1):
+        for rec in recs:  # a wave's records in log order
+            if rec[7] == w and rec[0] == 0 and rec[3] >= ne:
+                gathers.append((w, rec[3]))
+    consumed = {rec[2] for rec in recs} | {rec[3] for rec in recs}
+    gathers += [(n_waves + 1, e) for e in range(ne, len(src)) if e not in consumed]
+    return np.array(blk), np.array(first), np.array(local), gathers
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8])
+@pytest.mark.parametrize("graph", ["inception_chain", "vgg16", "series_parallel"])
+def test_shard_layout_matches_restatement(graph, nranks):
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import paper_1802_04924_b200 as P
+
+    g = P.series_parallel_graph(3, 300, 0.4) if graph == "series_parallel" else P.builtin_model(graph, 32)
+    counts = np.random.default_rng(nranks).integers(1, 700, g.n_layers).astype(np.int32)
+    covered = None
+    for rank in range(nranks):
+        blk, first, local, gathers = P.shard_layout(g, counts, nranks, rank)
+        rb, rf, rl, rg = _restated_layout(g, counts, nranks, rank)
+        assert (blk == rb).all() and (first == rf).all() and (local == rl).all()
+        assert gathers == rg
+        covered = local.copy() if covered is None else covered + local
+    # the ranks' row blocks tile every table exactly
+    recs, _ = g.schedule()
+    es, _, _ = g.edges()
+    src = list(es) + [rec[5] for rec in recs]
+    assert (covered == counts[np.array(src)]).all()
