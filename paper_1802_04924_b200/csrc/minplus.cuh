@@ -733,13 +733,13 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
   __syncthreads();
   if (warp == kMpConsumers / 32) { // producer: every fold's B'' stages, in order
     if (lane == 0) {
-      int64_t nn = 0;
+      int s = 0; // ring slot and its phase, advanced incrementally (5 stages: no division per stage)
+      unsigned ph = 0;
       for (int k = 0; k < K; ++k) {
         const MpFold &f = folds[k];
         const int stages = f.nchunks * (kMpChunk / kMpChainJ);
-        for (int st = 0; st < stages; ++st, ++nn) {
-          const int s = static_cast<int>(nn % kMpChainStages);
-          mbar_wait(&empty[s], (static_cast<unsigned>(nn / kMpChainStages) & 1u) ^ 1u);
+        for (int st = 0; st < stages; ++st, s = s + 1 == kMpChainStages ? (ph ^= 1u, 0) : s + 1) {
+          mbar_wait(&empty[s], ph ^ 1u);
           mbar_expect_tx(&full[s], kMpChainStageBytes);
           bulk_g2s(ch_smem + s * kMpChainStageBytes, f.B + static_cast<int64_t>(st) * kMpChainJ * kMpChainCols,
                    kMpChainStageBytes, &full[s]);
@@ -752,7 +752,8 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
   constexpr int SPG = (1 << JB) >= kMpChainJ ? (1 << JB) / kMpChainJ : 1; // stages per argmin group
   static_assert((1 << JB) >= kMpChainJ, "argmin groups span whole stages");
   const int c4 = tid * 4; // this thread's columns c4..c4+3
-  int64_t nn = 0;
+  int s = 0; // ring slot and phase (as the producer's)
+  unsigned ph = 0;
   for (int k = 0; k < K; ++k) {
     const MpFold &f = folds[k];
     const int r0 = static_cast<int>(blockIdx.x) * R, nr = min(R, f.nu - r0);
@@ -792,9 +793,8 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_chain_kernel(const MpFold *f
       m[r][0] = m[r][1] = 0xFFFFFFFFu;
     }
     const int stages = nwp / kMpChainJ;
-    for (int st = 0; st < stages; ++st, ++nn) {
-      const int s = static_cast<int>(nn % kMpChainStages);
-      mbar_wait(&full[s], static_cast<unsigned>(nn / kMpChainStages) & 1u);
+    for (int st = 0; st < stages; ++st, s = s + 1 == kMpChainStages ? (ph ^= 1u, 0) : s + 1) {
+      mbar_wait(&full[s], ph);
       const uint32_t *Bs = reinterpret_cast<const uint32_t *>(ch_smem + s * kMpChainStageBytes) + tid * 2;
       if (st % SPG == 0) {
 #pragma unroll
