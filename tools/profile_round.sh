@@ -3,9 +3,9 @@
 #   1. plain bench run (must exit 0 before any ncu pass)
 #   2. launch lists: the headline search (bench --quick) and the C=1024
 #      min-plus bench leg (per-launch gpu__time_duration, serialised)
-#   3. --set full of the min-plus kernels (a wide wave and a one-fold wave of
-#      mp_fold, mp_prep, mp_merge, mp_minima), the K1/K2 table build at I64 and
-#      the fused plan kernel (I16)
+#   3. --set full of the min-plus kernels (mp_fold on a wide and a narrow
+#      launch, mp_chain, mp_prep, mp_merge, mp_minima, the FP64 mp64_fold), the
+#      K1/K2 table build at I64 and the fused plan kernel (I16)
 set -e
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
@@ -21,8 +21,10 @@ full() { # name kernel-regex skip -- command
       > "gpurun_out/ncu_$name.log" 2>&1 || true
 }
 full mp_fold_wide_full mp_fold_kernel 0 -- python tools/mp_once.py 1024
-full mp_fold_full mp_fold_kernel 100 -- python tools/mp_once.py 1024
-full mp_prep_full mp_prep_kernel 100 -- python tools/mp_once.py 1024
+full mp_fold_full mp_fold_kernel 10 -- python tools/mp_once.py 1024
+full mp_chain_full mp_chain_kernel 0 -- python tools/mp_once.py 1024
+full mp64_fold_full mp64_fold_kernel 0 -- python tools/fp64_check.py 1024 120
+full mp_prep_full mp_prep_kernel 0 -- python tools/mp_once.py 1024
 full mp_merge_full mp_merge_kernel 0 -- python tools/mp_once.py 1024
 full mp_minima_full mp_minima_kernel 0 -- python tools/mp_once.py 1024
 full k1_build_i64_full build_tables_kernel 1 -- python tools/build_tables_once.py inception_chain@64
