@@ -454,11 +454,19 @@ def minplus_fp64(P, ctx, stream, C, check):
 def minplus(P, ctx, args, stream, sm_mhz):
     """Min-plus sweep; the headline roofline is the C=1024 point's mp_fold_kernel."""
     points = {}
+    import torch
+
+    def mem():
+        free, total = torch.cuda.mem_get_info()
+        return f"device memory free {free / 2**30:.1f} of {total / 2**30:.1f} GiB"
+
     for C in args.minplus_sweep:
+        ctx.release_pools()  # the previous point's one-shot (generic check) plan pool
+        torch.cuda.empty_cache()
         try:
             points[str(C)] = minplus_point(P, ctx, stream, C, args.minplus_runs, check=not args.no_check)
         except Exception as exc:  # report, keep the line
-            points[str(C)] = {"error": str(exc)[:300]}
+            points[str(C)] = {"error": str(exc)[:300] + "; " + mem()}
     f_mhz = sm_mhz or peaks().get("sm_max_mhz", 1965.0)
     peak_tflops = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # FP32 CUDA-core: 2 ops (add + min) per cell update per lane-clock
     for pt in points.values():
@@ -467,10 +475,12 @@ def minplus(P, ctx, args, stream, sm_mhz):
             pt["plan_frac"] = 2.0 * pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3) / 1e12 / peak_tflops
             pt["plan_cell_updates_per_s"] = pt["global_cell_updates"] / (pt["plan_ms"] * 1e-3)
     if args.fp64_c:
+        ctx.release_pools()
+        torch.cuda.empty_cache()
         try:
             points[f"fp64_{args.fp64_c}"] = minplus_fp64(P, ctx, stream, args.fp64_c, check=not args.no_check)
         except Exception as exc:
-            points[f"fp64_{args.fp64_c}"] = {"error": str(exc)[:300]}
+            points[f"fp64_{args.fp64_c}"] = {"error": str(exc)[:300] + "; " + mem()}
     head = points.get(str(args.minplus_c)) or next(iter(points.values()), {})
     traffic, basis = committed_traffic("mp_fold_kernel")
     roof = None
@@ -497,6 +507,7 @@ def sharded(P, args, local, stream, flush):
     from paper_1802_04924_b200 import distributed as PD
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    torch.cuda.empty_cache()
     sctx = P.Context(local, stream=stream.cuda_stream)
     PD.attach(sctx)
     out = {"ranks": world}

@@ -182,6 +182,9 @@ pp_status pp_vgroup_destroy(pp_vgroup *group);
 pp_status pp_shard_layout(const pp_graph *g, const int32_t *counts, int32_t nranks, int32_t rank, int32_t *n_tables,
                           int32_t *blk, int32_t *first, int32_t *local_rows, int32_t *n_gathers, int32_t *gather_wave,
                           int32_t *gather_table);
+/* One-shot plans draw on grow-only device pools (no cudaMalloc on the steady
+ * state path); this returns them to the device (e.g. after one very large plan). */
+pp_status pp_context_release_pools(pp_context *ctx);
 /* kernel launches issued on this context since creation */
 pp_status pp_context_launch_count(const pp_context *ctx, int64_t *launches);
 

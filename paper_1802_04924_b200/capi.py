@@ -91,6 +91,7 @@ _SIGS = {
     "pp_context_attach_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_char_p]),
     "pp_context_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "pp_vgroup_create": (C.c_int, [C.c_int32, C.c_int32, _pp]),
+    "pp_context_release_pools": (C.c_int, [_vp]),
     "pp_shard_layout": (C.c_int, [_vp, _i32p, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p]),
     "pp_vgroup_plan": (C.c_int, [_vp, _vp, C.c_void_p, _vp, C.c_int32, _i32p, C.POINTER(_PlanResult)]),
@@ -217,6 +218,10 @@ class Context:
         min-plus with proven caps only; '+'-joined combinations ('generic+unfused')."""
         bits = {"auto": 0, "generic": 1, "unfused": 2, "generic_unfused": 3, "conservative": 4}
         _check(lib().pp_context_set_kernel_policy(self.h, sum(bits[p] for p in policy.split("+"))))
+
+    def release_pools(self) -> None:
+        """Return the one-shot plan pools (grow-only) to the device."""
+        _check(lib().pp_context_release_pools(self.h))
 
     def attach_comm(self, nranks: int, rank: int, unique_id: bytes) -> None:
         """Join an NCCL communicator: plans on this context are row-sharded across ranks."""

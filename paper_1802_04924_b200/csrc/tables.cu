@@ -115,6 +115,18 @@ pp_status pp_context_stream(const pp_context *ctx, void **stream) {
   });
 }
 
+pp_status pp_context_release_pools(pp_context *ctx) {
+  return guard([&] {
+    PP_REQUIRE(ctx, "null context");
+    PP_CUDA(cudaSetDevice(ctx->device));
+    PP_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->plan_pool.release();
+    ctx->plan_scratch.release();
+    ctx->scratch.release();
+    ctx->last_pool_bytes = 0;
+  });
+}
+
 pp_status pp_context_destroy(pp_context *ctx) {
   if (!ctx) return PP_OK;
   cudaSetDevice(ctx->device);
