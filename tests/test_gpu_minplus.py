@@ -139,3 +139,26 @@ def test_fp64_large_fold_matches_fixed_point_on_dyadic_tables(gpu):
     a, b = P.plan_with_tables(g, t32), P.plan_with_tables(g, t64)
     assert a.precision == "fixed" and b.precision == "fp64"
     assert list(a.indices) == list(b.indices) and a.cost == b.cost
+
+
+@pytest.mark.parametrize("C,n", [(300, 40), (1000, 12), (130, 60)])
+def test_chain_runs_match_generic(gpu, C, n):
+    """A pure chain (one fold per wave, all t2 original): the whole run goes to
+    mp_chain (rows per CTA = ceil(C / 148), odd column counts, a last partial
+    row block) — same plan as the generic fold, and the C=300 tie-heavy variant."""
+    import paper_1802_04924_b200 as P
+
+    g = _chain(P, n)
+    rng = np.random.default_rng(C + n)
+    hi = 5 if C == 300 else 641  # C=300: values in [0, 4] -> many exact ties
+    counts = [C] * n
+    node, xfer = _tables(rng, counts, [(i, i + 1) for i in range(n - 1)], hi)
+    cat = [np.tile([1, 1, 1, 1], (c, 1)) for c in counts]
+    fast, slow = P.Context(0), P.Context(0)
+    slow.set_kernel_policy("generic")
+    tf = P.upload_cost_tables(g, cat, node, xfer, fast)
+    ts = P.upload_cost_tables(g, cat, node, xfer, slow)
+    kinds = [k for k, _, _ in P.PreparedPlan(g, tables=tf, ctx=fast).profile()]
+    assert "mp_chain" in kinds, kinds
+    a, b = P.plan_with_tables(g, tf), P.plan_with_tables(g, ts)
+    assert list(a.indices) == list(b.indices) and a.cost == b.cost
