@@ -707,8 +707,8 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp_fold_kernel(const MpFold *fo
 // arithmetic, caps and keys as mp_fold.
 constexpr int kMpChainCols = 1024;                     // columns per B'' row (nv <= 1024)
 constexpr int kMpChainRows = 8;                        // rows per CTA at most
-constexpr int kMpChainJ = 16;                          // j per stage
-constexpr int kMpChainStages = 5;
+constexpr int kMpChainJ = 32;                          // j per stage
+constexpr int kMpChainStages = 3;
 constexpr unsigned kMpChainStageBytes = kMpChainJ * kMpChainCols * 2; // 32 KiB
 constexpr int kMpChainNw = 1024;                       // padded nw at most (A in shared memory)
 constexpr size_t kMpChainSmem = kMpChainStages * kMpChainStageBytes + static_cast<size_t>(kMpChainNw) * kMpChainRows * 4 +

@@ -132,7 +132,7 @@ template <class T> void MinplusPlan::build(const In &in) {
         const int x0 = s.wave_begin[static_cast<size_t>(w)], x1 = s.wave_begin[static_cast<size_t>(w) + 1];
         const int oi = s.exec[static_cast<size_t>(x0)];
         const Op &op = s.ops[static_cast<size_t>(oi)];
-        const bool ok = x1 - x0 == 1 && large[static_cast<size_t>(oi)] && !op.type &&
+        const bool ok = x1 - x0 == 1 && large[static_cast<size_t>(oi)] && !op.type && fold_jb[static_cast<size_t>(oi)] >= 5 &&
                         cols[static_cast<size_t>(op.e2)] <= kMpChainCols &&
                         t.counts[static_cast<size_t>(op.removed)] <= kMpChainNw &&
                         rows[static_cast<size_t>(op.e1)] <= kMpChainRows * in.sms;

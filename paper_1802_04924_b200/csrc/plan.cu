@@ -173,7 +173,7 @@ using MpChainFn = void (*)(const MpFold *, int, int);
 // the chain kernel for a run: optimistic runs (JB 6) get the exact row count
 // per CTA, proven-cap runs (JB <= 5) the 8-row tile
 static MpChainFn mp_chain_launch(int jb, int R) {
-  if (jb < 6) return jb == 5 ? mp_chain_kernel<5, 8> : mp_chain_kernel<4, 8>;
+  if (jb < 6) return mp_chain_kernel<5, 8>; // runs need JB >= 5 (argmin groups cover whole stages)
   switch (R) {
   case 1: return mp_chain_kernel<6, 1>;
   case 2: return mp_chain_kernel<6, 2>;
@@ -357,7 +357,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   (void)mp_group;
   // dynamic shared memory allowances: per device, so set on every prepare (cheap)
   for (const MpRun &run : mp_runs)
-    for (int jb : {4, 5, 6})
+    for (int jb : {5, 6})
       PP_CUDA(cudaFuncSetAttribute(mp_chain_launch(jb, run.R), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(kMpChainSmem)));
   if (mp_part)
@@ -675,7 +675,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
             f.nchunks = L.nchunks;
             f.jb = fold_jb[static_cast<size_t>(oi)];
             for (int o2 : run.ops) f.jb = std::min(f.jb, fold_jb[static_cast<size_t>(o2)]); // one JB per run
-            f.jb = std::max(f.jb, 4);
+            f.jb = std::max(f.jb, 5);
             if (fold_opt[static_cast<size_t>(oi)]) {
               f.cap = mp_max_cap(f.jb);
               f.ovf = ovf_ptr();
