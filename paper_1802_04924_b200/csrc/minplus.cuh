@@ -34,9 +34,9 @@
 // not spanA + spanB, must fit: (2 cap << JB) + 2^JB - 1 <= 65534.  Static
 // bounds on derived tables are loose and minima of many candidates are small,
 // so folds run optimistically at JB = 6 (64-j groups: half the key updates of
-// JB = 5) with the largest JB-6 cap (511): the epilogue checks m'' < cap for
-// every stored cell and raises `ovf` otherwise, and the host then re-runs the
-// plan with the proven caps (JB <= 5).
+// JB = 5; the largest JB-6 cap, 511), or JB = 7 (cap 255) when nw >= 2048: the
+// epilogue checks m'' < cap for every stored cell and raises `ovf` otherwise,
+// and the host then re-runs the plan with the proven caps (JB <= 5).
 //
 // The group key must order (value, group, j mod 2^JB): per group and cell
 // pair, one LOP3 moves the two j-low fields next to the group id
@@ -131,7 +131,9 @@ inline int mp_jbits(int64_t M) {
     if (((2 * M + 2) << jb) + (1 << jb) - 1 <= 65534) return jb;
   return 0;
 }
-constexpr int kMpOptJB = 6; // optimistic plans: 64-j argmin groups, cap 511 (checked on the device)
+constexpr int kMpOptJB = 6;       // optimistic plans: 64-j argmin groups, cap 511 (checked on the device)
+constexpr int kMpOptJBWide = 7;   // folds with nw >= kMpWideNw: 128-j groups, cap 255 (minima of more candidates are smaller)
+constexpr int kMpWideNw = 2048;
 // the largest cap JB bits allow
 inline int32_t mp_max_cap(int jb) { return static_cast<int32_t>((65534 - ((1 << jb) - 1)) >> (jb + 1)); }
 

@@ -105,7 +105,7 @@ template <class T> void MinplusPlan::build(const In &in) {
       fold_m[oi] = std::min(t.node_span[static_cast<size_t>(op.removed)] + R[a], Kc[b2]);
       fold_jb[oi] = fold_m[oi] < 32768 ? mp_jbits(fold_m[oi]) : 0;
       // optimistic JB 6 (cap 511, checked in the epilogue) unless conservative
-      if (!conservative) fold_opt[oi] = 1, fold_jb[oi] = kMpOptJB;
+      if (!conservative) fold_opt[oi] = 1, fold_jb[oi] = nw >= kMpWideNw ? kMpOptJBWide : kMpOptJB;
       large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && fold_jb[oi] > 0 && !in.no_minplus;
       if (large[oi] && nu_eff(op.e1) > 0) {
         mp_consumer[a] = static_cast<int>(oi);
@@ -177,7 +177,7 @@ template <class T> void MinplusPlan::build(const In &in) {
     for (int w = 1; w <= s.n_waves; ++w) {
       size_t off = 0, coff = 0;
       int g = 0;
-      wave_group_jb[static_cast<size_t>(w)].assign(1, kMpOptJB);
+      wave_group_jb[static_cast<size_t>(w)].assign(1, kMpOptJBWide);
       for (int x = s.wave_begin[static_cast<size_t>(w)]; x < s.wave_begin[static_cast<size_t>(w) + 1]; ++x) {
         const int oi = s.exec[static_cast<size_t>(x)];
         if (!large[static_cast<size_t>(oi)] || run_of[static_cast<size_t>(oi)] >= 0) continue;
@@ -196,7 +196,7 @@ template <class T> void MinplusPlan::build(const In &in) {
           cnt = std::max(cnt, coff);
           off = coff = 0;
           ++g;
-          wave_group_jb[static_cast<size_t>(w)].push_back(kMpOptJB);
+          wave_group_jb[static_cast<size_t>(w)].push_back(kMpOptJBWide);
         }
         mp_group[static_cast<size_t>(oi)] = g;
         int &gjb = wave_group_jb[static_cast<size_t>(w)].back();

@@ -173,16 +173,16 @@ using MpChainFn = void (*)(const MpFold *, int, int);
 // the chain kernel for a run: optimistic runs (JB 6) get the exact row count
 // per CTA, proven-cap runs (JB <= 5) the 8-row tile
 static MpChainFn mp_chain_launch(int jb, int R) {
-  if (jb < 6) return mp_chain_kernel<5, 8>; // runs need JB >= 5 (argmin groups cover whole stages)
+  if (jb < kMpOptJB) return mp_chain_kernel<5, 8>; // runs need JB >= 5 (argmin groups cover whole stages)
   switch (R) {
-  case 1: return mp_chain_kernel<6, 1>;
-  case 2: return mp_chain_kernel<6, 2>;
-  case 3: return mp_chain_kernel<6, 3>;
-  case 4: return mp_chain_kernel<6, 4>;
-  case 5: return mp_chain_kernel<6, 5>;
-  case 6: return mp_chain_kernel<6, 6>;
-  case 7: return mp_chain_kernel<6, 7>;
-  default: return mp_chain_kernel<6, 8>;
+  case 1: return mp_chain_kernel<kMpOptJB, 1>;
+  case 2: return mp_chain_kernel<kMpOptJB, 2>;
+  case 3: return mp_chain_kernel<kMpOptJB, 3>;
+  case 4: return mp_chain_kernel<kMpOptJB, 4>;
+  case 5: return mp_chain_kernel<kMpOptJB, 5>;
+  case 6: return mp_chain_kernel<kMpOptJB, 6>;
+  case 7: return mp_chain_kernel<kMpOptJB, 7>;
+  default: return mp_chain_kernel<kMpOptJB, 8>;
   }
 }
 
@@ -357,11 +357,11 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
   (void)mp_group;
   // dynamic shared memory allowances: per device, so set on every prepare (cheap)
   for (const MpRun &run : mp_runs)
-    for (int jb : {5, 6})
+    for (int jb : {5, kMpOptJB})
       PP_CUDA(cudaFuncSetAttribute(mp_chain_launch(jb, run.R), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(kMpChainSmem)));
   if (mp_part)
-    for (auto fn : {mp_fold_kernel<6>, mp_fold_kernel<5>, mp_fold_kernel<4>, mp_fold_kernel<3>})
+    for (auto fn : {mp_fold_kernel<7>, mp_fold_kernel<6>, mp_fold_kernel<5>, mp_fold_kernel<4>, mp_fold_kernel<3>})
       PP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMpSmem)));
   if (mp_bytes && std::is_same_v<T, double>)
     PP_CUDA(cudaFuncSetAttribute(mp64_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMp64Smem)));
@@ -1420,7 +1420,8 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         PP_CUDA(cudaLaunchKernelEx(&cfg,
-                                   jb == 6   ? mp_fold_kernel<6>
+                                   jb == 7   ? mp_fold_kernel<7>
+                                   : jb == 6 ? mp_fold_kernel<6>
                                    : jb == 5 ? mp_fold_kernel<5>
                                    : jb == 4 ? mp_fold_kernel<4>
                                              : mp_fold_kernel<3>,
@@ -1698,6 +1699,7 @@ static void launch(pp_prepared *P, bool upload);
 // (plan_with_tables), so no table build is repeated.
 static void rerun_conservative(pp_prepared *P) {
   PP_CUDA(cudaEventSynchronize(P->ctx->ev1));
+  if (std::getenv("PARPLAN_TRACE")) std::fprintf(stderr, "[parplan] optimistic operand cap reached: re-planning with proven caps\n");
   P->mp_conservative = true;
   build_steps<int32_t>(P, nullptr, P->k_bound);
   P->uploaded = false;
