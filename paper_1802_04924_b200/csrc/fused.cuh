@@ -127,7 +127,10 @@ __device__ __forceinline__ void stage_item(const FusedWave<T> &W, int ready, Pan
   }
 }
 
-template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_kernel(FusedArgs<T> a) {
+// kBuild: the image holds the K1/K2 phase.  Plans whose tables are built by a
+// separate launch (one-shot plans build them while the host prepares the DP
+// image) run the variant without it: a ~25 % smaller instruction image.
+template <class T, bool kBuild> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_kernel(FusedArgs<T> a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   // dynamic: max(WaveSmem, the largest chain item) bytes
@@ -144,7 +147,7 @@ template <class T> __global__ void __launch_bounds__(kFusedThreads, 2) dp_fused_
   int ph = 0;
   if (stamp) a.stamps[ph++] = global_ns();
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 2048) a.trace[16 * a.n_waves + 16 + 2048 + blockIdx.x] = global_ns();
-  if (a.has_build) {
+  if (kBuild && a.has_build) {
     const BuildArgs &B = a.build;
     const int64_t n = B.ncells + a.xcells;
     // the binary searches over layers and edges read their offsets from

@@ -40,7 +40,7 @@ struct Knobs {
       chain_min_waves, early_build, grid_barrier, build_dynamic, panel,
       panel_side, chains,
       chain_path, rotate,
-      wave_trace, stage, blocks_per_sm;
+      wave_trace, stage, blocks_per_sm, split_build;
   Knobs()
       : cluster(env_int("PARPLAN_CLUSTER", 1)), narrow_items(env_int("PARPLAN_NARROW_ITEMS", 0)),
         chain_smem_kb(env_int("PARPLAN_CHAIN_SMEM_KB", 110)), chain_smem_big_kb(env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216)),
@@ -53,7 +53,7 @@ struct Knobs {
         panel_side(env_int("PARPLAN_PANEL_SIDE", 0)), chains(env_int("PARPLAN_CHAINS", 1)),
         chain_path(env_int("PARPLAN_CHAIN_PATH", 1)), rotate(env_int("PARPLAN_ROTATE", 1)),
         wave_trace(env_int("PARPLAN_WAVE_TRACE", 0)), stage(env_int("PARPLAN_STAGE", 1)),
-        blocks_per_sm(env_int("PARPLAN_FUSED_BLOCKS_PER_SM", 0)) {}
+        blocks_per_sm(env_int("PARPLAN_FUSED_BLOCKS_PER_SM", 0)), split_build(env_int("PARPLAN_SPLIT_BUILD", 1)) {}
 };
 }
 
@@ -1251,7 +1251,10 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
     ba.node_blocks = static_cast<int32_t>(bp->node_blocks);
     ba.bw_uniform = bp->bw_uniform;
   }
-  if (bp && bp->grid > 0 && !use_fused && !shard) {
+  // fused plans may build their tables in a separate launch before the DP
+  // kernel (PARPLAN_SPLIT_BUILD): the DP kernel then runs without the K1/K2 code
+  const bool split_build = use_fused && bp && bp->grid > 0 && !early && kn.split_build;
+  if (bp && bp->grid > 0 && (!use_fused || split_build) && !shard) {
     const BuildArgs a = ba;
     const int64_t grid = bp->grid;
     P->steps.push_back([ctx, a, grid](cudaStream_t st) { launch_build(ctx, st, a, grid); });
@@ -1507,9 +1510,9 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       launches += 2;
     } else {
       FusedArgs<T> fz{};
-      fz.has_build = bp != nullptr && !early;
+      fz.has_build = bp != nullptr && !early && !split_build;
       fz.build = ba;
-      fz.xcells = bp && !early ? t.xcells : 0;
+      fz.xcells = fz.has_build ? t.xcells : 0;
       fz.waves = reinterpret_cast<const FusedWave<T> *>(dimg + im.oFW);
       fz.n_waves = static_cast<int32_t>(im.n_phases);
       fz.en = en, fz.ee = ee, fz.k = K, fz.m = m;
@@ -1534,6 +1537,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       P->phase_chain = im.phase_chain;
       clk.mark("steps");
       const size_t dyn = im.dyn_smem;
+      void (*const fused_fn)(FusedArgs<T>) = fz.has_build ? dp_fused_kernel<T, true> : dp_fused_kernel<T, false>;
       {
         // grow the dynamic allowance monotonically; keep the shared-memory
         // carveout at what two co-resident blocks need (the rest stays L1,
@@ -1541,24 +1545,25 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         // function attributes are per device: the allowance only ever grows,
         // tracked per device under a lock (several contexts / threads)
         static std::mutex mu;
-        static std::map<int, std::array<size_t, 2>> dev_set;
+        static std::map<int, std::array<size_t, 4>> dev_set; // per (T, with build phase)
         std::lock_guard<std::mutex> lock(mu);
         size_t *dyn_set = dev_set[ctx->device].data();
-        if (dyn_set[sizeof(T) == 8] < dyn) {
-          PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+        const int fi = (sizeof(T) == 8 ? 2 : 0) + (fz.has_build ? 1 : 0);
+        if (dyn_set[fi] < dyn) {
+          PP_CUDA(cudaFuncSetAttribute(fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
           cudaFuncAttributes fa_{};
-          PP_CUDA(cudaFuncGetAttributes(&fa_, dp_fused_kernel<T>));
+          PP_CUDA(cudaFuncGetAttributes(&fa_, fused_fn));
           const double need = 2.0 * static_cast<double>(dyn + fa_.sharedSizeBytes + 1024);
           const int pct = std::min(100, static_cast<int>(std::ceil(100.0 * need / (228.0 * 1024))));
-          PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-          dyn_set[sizeof(T) == 8] = dyn;
+          PP_CUDA(cudaFuncSetAttribute(fused_fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+          dyn_set[fi] = dyn;
         }
       }
       int occ = 0;
-      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_fused_kernel<T>, kFusedThreads, dyn));
+      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_fn, kFusedThreads, dyn));
       PP_REQUIRE(occ > 0, "fused plan kernel does not fit on an SM");
       int64_t items = std::max<int64_t>(nblk, 1);
-      if (bp && !early) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
+      if (fz.has_build) items = std::max<int64_t>(items, (t.ncells + t.xcells + kFusedThreads - 1) / kFusedThreads);
       for (const auto &wr : im.waves) items = std::max<int64_t>(items, wr.ftiles + wr.mblocks);
       const int per_sm_env = kn.blocks_per_sm;
       const int per_sm = per_sm_env > 0 ? std::min(per_sm_env, occ) : occ;
@@ -1571,7 +1576,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       attr[1].val.clusterDim.x = static_cast<unsigned>(nc), attr[1].val.clusterDim.y = 1, attr[1].val.clusterDim.z = 1;
       int64_t cap = int64_t(ctx->sms) * per_sm;
       if (nc > 1) {
-        PP_CUDA(cudaFuncSetAttribute(dp_fused_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        PP_CUDA(cudaFuncSetAttribute(fused_fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cudaLaunchConfig_t q{};
         q.gridDim = dim3(static_cast<unsigned>(nc));
         q.blockDim = dim3(kFusedThreads);
@@ -1579,7 +1584,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         q.numAttrs = 2;
         q.dynamicSmemBytes = dyn;
         int clusters = 0;
-        PP_CUDA(cudaOccupancyMaxActiveClusters(&clusters, dp_fused_kernel<T>, &q));
+        PP_CUDA(cudaOccupancyMaxActiveClusters(&clusters, fused_fn, &q));
         PP_REQUIRE(clusters > 0, "fused plan kernel: no co-resident cluster of " + std::to_string(nc));
         cap = std::min<int64_t>(cap, int64_t(clusters) * nc) / nc * nc;
       }
@@ -1587,7 +1592,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
       const int64_t want = (items + nc - 1) / nc * nc;
       const unsigned grid = static_cast<unsigned>(std::max<int64_t>(nc, std::min<int64_t>(want, cap)));
       fz.nc = nc;
-      P->steps.push_back([ctx, fz, grid, attr, dyn, nc](cudaStream_t st) {
+      P->steps.push_back([ctx, fz, grid, attr, dyn, nc, fused_fn](cudaStream_t st) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kFusedThreads);
@@ -1595,7 +1600,7 @@ static void build_steps(pp_prepared *P, const BuildPlan *bp, int k_bound) {
         cfg.stream = st;
         cfg.attrs = const_cast<cudaLaunchAttribute *>(attr);
         cfg.numAttrs = nc > 1 ? 2 : 1;
-        PP_CUDA(cudaLaunchKernelEx(&cfg, dp_fused_kernel<T>, fz));
+        PP_CUDA(cudaLaunchKernelEx(&cfg, fused_fn, fz));
         check_launch(ctx);
       });
       P->step_kind.push_back(10);

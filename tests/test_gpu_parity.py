@@ -118,7 +118,8 @@ def test_prepared_plan_and_profile(gpu):
     kinds = [k for k, _, _ in prof]
     # one phase per wave, except chain segments (several waves, one phase)
     phases = kinds.count("fused.wave") + kinds.count("fused.chain")
-    assert kinds[0] == "fused.tables" and 1 <= phases <= r.waves and kinds[-1] == "fused"
+    # the table build: its own launch (default) or the fused kernel's first phase
+    assert kinds[0] in ("tables", "fused.tables") and 1 <= phases <= r.waves and kinds[-1] == "fused"
     assert sum(w for k, _, w in prof if k in ("fused.wave", "fused.chain")) > 0
 
 
@@ -236,6 +237,7 @@ def test_evaluate_batch_matches_oracle(gpu, source):
 # plan — the hand-rolled barrier vs grid.sync(), dynamic vs static build chunks,
 # chain segments and merge absorption off, the early table build off
 KNOBS = [{"PARPLAN_GRID_BARRIER": "0"}, {"PARPLAN_BUILD_DYNAMIC": "0"}, {"PARPLAN_CHAINS": "0"},
+         {"PARPLAN_SPLIT_BUILD": "0"}, {"PARPLAN_SPLIT_BUILD": "0", "PARPLAN_BUILD_DYNAMIC": "0"},
          {"PARPLAN_MERGE_FUSE": "0"}, {"PARPLAN_EARLY_BUILD": "0"}, {"PARPLAN_STAGE": "0", "PARPLAN_PANEL": "0"},
          # narrow waves on the first thread-block cluster (cluster barriers between
          # consecutive narrow waves; the staging-visibility rule of plan.cu's `seen`)
