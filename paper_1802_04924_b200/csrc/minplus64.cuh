@@ -35,8 +35,8 @@ struct Mp64Fold {
   uint16_t *am;
   double *A, *B;
   int32_t nu, nw, nv, tiles_i, tiles_k, nchunks;
-  int64_t prep_begin; // A prep blocks (row groups of 32), then B prep blocks (chunk rows)
-  int32_t prep_a;
+  int64_t prep_begin; // A prep blocks (row groups of 32 x chunk groups), then B prep blocks (chunk x tile groups)
+  int64_t prep_a;
   int64_t tile_begin; // first mp64_fold block
 };
 
@@ -52,8 +52,18 @@ __device__ __forceinline__ int find64(const Mp64Fold *d, int n, int64_t b, bool 
   return lo;
 }
 
-// A block: 32 rows x all chunks (32x32 tiles through shared memory, transposed);
-// B block: one 32-j chunk row of t2 for all column tiles.
+// A blocks: 32 rows x kMp64PrepChunks chunks (32x32 tiles transposed through
+// shared memory); B blocks: one 32-j chunk of t2 x kMp64PrepTiles column tiles.
+// Enough blocks per fold to keep every SM streaming (HBM-bound copy).
+constexpr int kMp64PrepChunks = 4;
+constexpr int kMp64PrepTiles = 4;
+__host__ __device__ inline int64_t mp64_prep_a_blocks(int nu, int nchunks) {
+  return static_cast<int64_t>((nu + 31) / 32) * ((nchunks + kMp64PrepChunks - 1) / kMp64PrepChunks);
+}
+__host__ __device__ inline int64_t mp64_prep_b_blocks(int nchunks, int tiles_k) {
+  return static_cast<int64_t>(nchunks) * ((tiles_k + kMp64PrepTiles - 1) / kMp64PrepTiles);
+}
+
 __global__ void __launch_bounds__(256) mp64_prep_kernel(const Mp64Fold *folds, int n) {
   const int64_t b = blockIdx.x;
   const Mp64Fold &f = folds[find64(folds, n, b, false)];
@@ -61,11 +71,13 @@ __global__ void __launch_bounds__(256) mp64_prep_kernel(const Mp64Fold *folds, i
   const int tid = threadIdx.x;
   if (pb < f.prep_a) {
     __shared__ double tr[32][33];
-    const int i0 = static_cast<int>(pb) * 32, ti = i0 / kMp64Tile, ii0 = i0 % kMp64Tile;
+    const int ncg = (f.nchunks + kMp64PrepChunks - 1) / kMp64PrepChunks;
+    const int i0 = static_cast<int>(pb / ncg) * 32, ti = i0 / kMp64Tile, ii0 = i0 % kMp64Tile;
+    const int c0 = static_cast<int>(pb % ncg) * kMp64PrepChunks, c1 = min(f.nchunks, c0 + kMp64PrepChunks);
     const int lr = tid >> 3, lj = (tid & 7) * 4; // load: row lr, j lj..lj+3
     const int sj = tid >> 3, sr = (tid & 7) * 4; // store: j sj, rows sr..sr+3
     const int i = i0 + lr;
-    for (int c = 0; c < f.nchunks; ++c) {
+    for (int c = c0; c < c1; ++c) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int j = c * kMp64Chunk + lj + e;
@@ -80,13 +92,17 @@ __global__ void __launch_bounds__(256) mp64_prep_kernel(const Mp64Fold *folds, i
     }
     return;
   }
-  const int64_t bb = pb - f.prep_a; // chunk c: rows j of all column tiles
-  const int c = static_cast<int>(bb);
-  for (int x = tid; x < kMp64Chunk * f.tiles_k * kMp64Tile; x += 256) {
-    const int jj = x / (f.tiles_k * kMp64Tile), k = x - jj * (f.tiles_k * kMp64Tile);
-    const int j = c * kMp64Chunk + jj, tk = k / kMp64Tile;
-    f.B[(static_cast<int64_t>(tk) * f.nchunks + c) * (kMp64Chunk * kMp64Tile) + jj * kMp64Tile + (k - tk * kMp64Tile)] =
-        j < f.nw && k < f.nv ? f.t2[static_cast<int64_t>(j) * f.nv + k] : 0.0;
+  // B: chunk c, column tiles [t0, t0 + kMp64PrepTiles): each thread one column, all 32 j
+  const int64_t bb = pb - f.prep_a;
+  const int ntg = (f.tiles_k + kMp64PrepTiles - 1) / kMp64PrepTiles;
+  const int c = static_cast<int>(bb / ntg), t0 = static_cast<int>(bb % ntg) * kMp64PrepTiles;
+  const int k = t0 * kMp64Tile + tid, tk = k / kMp64Tile;
+  if (tk >= f.tiles_k) return;
+  double *dst = f.B + (static_cast<int64_t>(tk) * f.nchunks + c) * (kMp64Chunk * kMp64Tile) + (k - tk * kMp64Tile);
+#pragma unroll 4
+  for (int jj = 0; jj < kMp64Chunk; ++jj) {
+    const int j = c * kMp64Chunk + jj;
+    dst[jj * kMp64Tile] = j < f.nw && k < f.nv ? f.t2[static_cast<int64_t>(j) * f.nv + k] : 0.0;
   }
 }
 
