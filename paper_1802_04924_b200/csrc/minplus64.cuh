@@ -5,8 +5,9 @@
 // (planner.hpp:139-155): the first add is done once per (i, j) in the prep
 // (the same IEEE rounding), the second per cell; strict '<' over ascending j
 // keeps the lowest index among equal candidates.  64x64 output tile per CTA,
-// 4x4 cells per thread: per j, 16 DADD + 16 DSETP on the FP64 pipe and three
-// selects per cell (value halves and j); operands staged by bulk copies
+// 4x4 cells per thread: per j, 16 DADD + 16 DSETP on the FP64 pipe, per cell
+// two predicated IMADs (the value halves, FMA pipe) and one select (j, ALU);
+// operands staged by bulk copies
 // (thread 0, mbarrier ring) from per-(tile, 32-j chunk) contiguous blocks.
 //
 //   mp64_prep  a = w + t1 -> A [tile_i][chunk][32 j][64 i]  (+inf for padded j)
@@ -35,6 +36,7 @@ struct Mp64Fold {
   uint16_t *am;
   double *A, *B;
   int32_t nu, nw, nv, tiles_i, tiles_k, nchunks;
+  int32_t one; // 1 (a value the compiler cannot fold: the fold's predicated IMAD selects)
   int64_t prep_begin; // A prep blocks (row groups of 32 x chunk groups), then B prep blocks (chunk x tile groups)
   int64_t prep_a;
   int64_t tile_begin; // first mp64_fold block
@@ -131,12 +133,16 @@ __global__ void __launch_bounds__(kMp64Threads, 2) mp64_fold_kernel(const Mp64Fo
   };
   if (tid == 0)
     for (int c = 0; c < kMp64Stages - 1 && c < f.nchunks; ++c) issue(c);
-  double best[4][4];
-  int bj[4][4];
+  // best value (as its two 32-bit halves) and argmin per cell.  The value
+  // selects are predicated IMADs by a runtime 1 (f.one): they issue on the FMA
+  // pipe, which is otherwise idle, instead of two ALU selects per cell (ptxas
+  // keeps the j update a select; measured best among the variants tried)
+  uint32_t blo[4][4], bhi[4][4], bj[4][4];
+  const uint32_t one = static_cast<uint32_t>(f.one);
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) best[r][q] = __longlong_as_double(0x7ff0000000000000LL), bj[r][q] = 0;
+    for (int q = 0; q < 4; ++q) blo[r][q] = 0u, bhi[r][q] = 0x7ff00000u, bj[r][q] = 0u;
   for (int c = 0; c < f.nchunks; ++c) {
     const int s = c % kMp64Stages;
     // the stage refilled below was last read in iteration c - 1: every thread is past it
@@ -161,7 +167,16 @@ __global__ void __launch_bounds__(kMp64Threads, 2) mp64_fold_kernel(const Mp64Fo
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const double cand = __dadd_rn(a[r], bv[q]);
-          if (cand < best[r][q]) best[r][q] = cand, bj[r][q] = j; // strict: the lowest j wins ties
+          // strict: the lowest j wins ties
+          asm("{\n\t.reg .pred p;\n\t.reg .f64 b;\n\t.reg .b32 cl, ch;\n\t"
+              "mov.b64 b, {%0, %1};\n\t"
+              "mov.b64 {cl, ch}, %3;\n\t"
+              "setp.lt.f64 p, %3, b;\n\t"
+              "@p mad.lo.u32 %0, cl, %5, 0;\n\t"
+              "@p mad.lo.u32 %1, ch, %5, 0;\n\t"
+              "@p mad.lo.u32 %2, %4, %5, 0;\n\t}"
+              : "+r"(blo[r][q]), "+r"(bhi[r][q]), "+r"(bj[r][q])
+              : "d"(cand), "r"(static_cast<uint32_t>(j)), "r"(one));
         }
     }
   }
@@ -173,7 +188,8 @@ __global__ void __launch_bounds__(kMp64Threads, 2) mp64_fold_kernel(const Mp64Fo
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (k0 + q < f.nv) {
-        f.out[static_cast<int64_t>(i) * f.nv + k0 + q] = best[r][q];
+        f.out[static_cast<int64_t>(i) * f.nv + k0 + q] =
+            __hiloint2double(static_cast<int>(bhi[r][q]), static_cast<int>(blo[r][q]));
         f.am[static_cast<int64_t>(i) * f.nv + k0 + q] = static_cast<uint16_t>(bj[r][q]);
       }
   }

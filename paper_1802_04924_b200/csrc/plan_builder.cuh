@@ -541,6 +541,7 @@ template <class T> void PlanBuilder<T>::image_waves(Image &im, Work &wk) {
           f.tiles_i = (f.nu + kMp64Tile - 1) / kMp64Tile;
           f.tiles_k = (f.nv + kMp64Tile - 1) / kMp64Tile;
           f.nchunks = (f.nw + kMp64Chunk - 1) / kMp64Chunk;
+          f.one = 1;
           f.prep_a = mp64_prep_a_blocks(f.nu, f.nchunks);
           f.prep_begin = G.prep_blocks;
           G.prep_blocks += f.prep_a + mp64_prep_b_blocks(f.nchunks, f.tiles_k);
