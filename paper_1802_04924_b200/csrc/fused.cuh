@@ -32,6 +32,7 @@ template <class T> struct FusedWave {
   const ChainDesc *chains;
   int64_t stage;    // chain segment: bytes per staging buffer
   const FoldDesc<T> *cfolds;
+  const uint16_t *fold_of; // per fold tile: its fold in `folds` (null: binary search)
 };
 
 __device__ __forceinline__ int64_t first_item(int64_t rot) {
@@ -114,7 +115,7 @@ __device__ __forceinline__ void stage_item(const FusedWave<T> &W, int ready, Pan
     return;
   }
   if (b < W.ftiles) {
-    const FoldDesc<T> f = W.folds[find_fold(W.folds, W.nf, b)];
+    const FoldDesc<T> f = W.folds[find_fold(W.folds, W.nf, b, W.fold_of)];
     int mask = 0;
     if (panel_fold(f)) {
       mask = (kPanelAll & ~f.late) | ready;
@@ -225,7 +226,8 @@ template <class T, bool kBuild> __global__ void __launch_bounds__(kFusedThreads,
       for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x) chain_item<T>(W.chains, W.n_chains, W.cfolds, it, fused_smem, static_cast<size_t>(W.stage));
     else if (!narrow || static_cast<int>(blockIdx.x) < a.nc)
       for (int64_t it = b0; it < W.items; it += step)
-        wave_item<T>(W.folds, W.nf, W.ftiles, W.merges, W.nm, it, sm, narrow ? nullptr : &st, it == 0 ? tr : nullptr);
+        wave_item<T>(W.folds, W.nf, W.ftiles, W.merges, W.nm, it, sm, narrow ? nullptr : &st, it == 0 ? tr : nullptr,
+                     W.fold_of);
     bool next_narrow = false;
     if (w + 1 < a.n_waves) {
       W = a.waves[w + 1];

@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <climits>
+#include <type_traits>
 
 namespace pp {
 
@@ -547,7 +548,12 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
   }
 }
 
-template <class T> __device__ __forceinline__ int find_fold(const FoldDesc<T> *folds, int n_folds, int64_t b) {
+// fold of work item b: the wave's per-tile fold index when the image has one
+// (fused plans: one load instead of a chain of dependent ones), else a binary
+// search over the folds' first tiles
+template <class T>
+__device__ __forceinline__ int find_fold(const FoldDesc<T> *folds, int n_folds, int64_t b, const uint16_t *fold_of = nullptr) {
+  if (fold_of) return fold_of[b];
   int lo = 0, hi = n_folds - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -576,12 +582,13 @@ template <class T> __device__ __forceinline__ int find_merge(const MergeDesc<T> 
 template <class T>
 __device__ __forceinline__ void wave_item(const FoldDesc<T> *folds, int n_folds, int64_t fold_tiles,
                                           const MergeDesc<T> *merges, int n_merges, int64_t b, WaveSmem<T> &sm,
-                                          const StagedItem<T> *pre = nullptr, uint64_t *tr = nullptr) {
+                                          const StagedItem<T> *pre = nullptr, uint64_t *tr = nullptr,
+                                          const uint16_t *fold_of = nullptr) {
   auto &As = sm.t.As;
   auto &Bs = sm.t.Bs;
   const bool staged = pre && pre->b == b;
   if (b < fold_tiles) {
-    const FoldDesc<T> f = staged ? pre->f : folds[find_fold(folds, n_folds, b)];
+    const FoldDesc<T> f = staged ? pre->f : folds[find_fold(folds, n_folds, b, fold_of)];
     const int64_t tile = b - f.tile_begin;
     if (panel_fold(f)) {
       panel_tile<T>(f, tile, staged ? pre->mask : 0, sm.p, tr);

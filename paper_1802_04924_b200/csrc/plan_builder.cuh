@@ -830,6 +830,16 @@ template <class T> void PlanBuilder<T>::image_phases(Image &im, Work &wk) {
     }
     const int64_t items = wr.ftiles + wr.mblocks;
     FusedWave<T> e{};
+    if (wr.nf > 1) { // per-tile fold index (replaces a binary search per work item)
+      std::vector<uint16_t> fold_of(static_cast<size_t>(wr.ftiles));
+      PP_REQUIRE(wr.nf <= 65535, "too many folds in one wave");
+      for (int q = 0; q < wr.nf; ++q) {
+        const int64_t t0 = wk.folds[wr.f0 + static_cast<size_t>(q)].tile_begin;
+        const int64_t t1 = q + 1 < wr.nf ? wk.folds[wr.f0 + static_cast<size_t>(q) + 1].tile_begin : wr.ftiles;
+        for (int64_t x = t0; x < t1; ++x) fold_of[static_cast<size_t>(x)] = static_cast<uint16_t>(q);
+      }
+      e.fold_of = reinterpret_cast<const uint16_t *>(db + off_image + pk.put(fold_of));
+    }
     e.folds = reinterpret_cast<const FoldDesc<T> *>(db + off_image + im.oF) + wr.f0;
     e.merges = reinterpret_cast<const MergeDesc<T> *>(db + off_image + im.oM) + wr.m0;
     e.nf = wr.nf, e.nm = wr.nm, e.ftiles = wr.ftiles, e.items = items, e.rot = rot;
