@@ -623,6 +623,19 @@ def run_ours(args):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_ms = e2e_t.item() / (args.steps * world)
     assert list(res.indices) == list(r.indices) and res.cost == r.cost
+    # the same call with the plan cache off: every call prepares from scratch
+    # (catalogs and schedule still cached per graph)
+    os.environ["PARPLAN_PLAN_CACHE"] = "0"
+    e2e_nc = []
+    for k in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = P.plan(g, dev, ctx=ctx)
+        if k >= args.warmup:
+            e2e_nc.append((time.perf_counter() - t0) * 1e3)
+    del os.environ["PARPLAN_PLAN_CACHE"]
+    assert list(res.indices) == list(r.indices) and res.cost == r.cost
 
     # ---- per-kernel breakdown of the search -----------------------------------------
     prof = prep.profile()
@@ -650,8 +663,11 @@ def run_ours(args):
         "config_detail": {"layers": g.n_layers, "edges": g.n_edges, "l2": "256 MiB write between timed steps",
                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "call": "pp_plan(ctx, graph, device_desc, k_bound, host indices) on a cached pp_graph: host prep + "
-                        "H2D + device + D2H (see dropin_e2e for parplan::plan() with a fresh graph per call)"},
+                "call": "pp_plan(ctx, graph, device_desc, k_bound, host indices), repeated: the library's plan "
+                        "cache replays a prepared plan -- H2D of the descriptor image (graph + device inputs), "
+                        "table build, search, D2H of the result every call (see dropin_e2e for parplan::plan() "
+                        "with a fresh graph per call)",
+                "no_plan_cache_ms": statistics.mean(e2e_nc)},
         "gpu_launches": launches,
         "plan_with_tables_ms": statistics.mean(pw),
         "result": {"cost": r.cost, "node_eliminations": r.node_eliminations, "edge_eliminations": r.edge_eliminations,

@@ -250,7 +250,12 @@ pp_status pp_tables_build_ms(const pp_tables *t, double *ms);
 
 /* ---- planning (device) -------------------------------------------------- */
 /* plan() (planner.hpp:368-371): tables + reduce + enumerate_final + unwind.
- * indices[n_layers] receives the config index per layer. */
+ * indices[n_layers] receives the config index per layer.  A call repeated on
+ * the same context with an equal graph, device description, k_bound, kernel
+ * policy and knobs replays a prepared plan the context keeps (at most 4, LRU;
+ * freed by pp_context_release_pools / pp_context_destroy): the descriptor image
+ * is uploaded and the tables and the search rerun on the device every call.
+ * PARPLAN_PLAN_CACHE=0 disables it. */
 pp_status pp_plan(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev, int32_t k_bound, int32_t *indices,
                   pp_plan_result *res);
 /* plan_with_tables() (planner.hpp:339-366) */

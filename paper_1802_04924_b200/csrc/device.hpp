@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -123,6 +124,8 @@ struct pp_context {
   size_t last_image_bytes = 0;          // reserve hint for the next descriptor image
   size_t last_pool_bytes = 0;           // largest one-shot plan pool so far (early table builds)
   pp::DBuf<unsigned int> gbar;          // fused kernel: grid-barrier word [0], build chunk counter [32..33] (zeroed once)
+  // prepared plans of repeated one-shot pp_plan calls (plan.cu PlanCache)
+  std::shared_ptr<void> plan_cache;
 
   void begin() const; // cudaSetDevice + record ev0
   double end_ms();    // record ev1, sync, elapsed

@@ -18,6 +18,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
 
 using namespace pp;
 
@@ -195,6 +198,86 @@ void run_plan(pp_context *ctx, Graph &g, Tables *t, const pp_device_desc *dev, i
   }
 }
 
+// ---- plan cache of one-shot pp_plan calls --------------------------------------
+// A reference caller re-plans the same model on the same devices
+// (parplan::plan(graph, devices) per request, planner.hpp:368-371).  The second
+// call with the same graph (content-addressed: equal graphs share one Graph),
+// device description, k_bound, kernel policy and knobs keeps a prepared plan
+// (its own memory and captured CUDA graph).  Later calls upload its descriptor
+// image -- the inputs: layer / edge descriptors, configs, rates, bandwidths --
+// and replay it: the device rebuilds the cost tables and reruns the whole
+// search every call.  Only the host-side preparation is reused.
+// PARPLAN_PLAN_CACHE=0 disables it.
+struct PlanCache {
+  struct Entry {
+    std::string key;
+    std::shared_ptr<Graph> g; // keeps the Graph (and so the key's address) alive
+    std::unique_ptr<pp_prepared> P;
+    uint64_t used = 0;
+  };
+  std::vector<Entry> entries;
+  std::vector<std::string> seen; // keys planned once: a second call caches
+  uint64_t tick = 0;
+};
+constexpr size_t kPlanCacheEntries = 4;
+constexpr size_t kPlanCacheMaxBytes = size_t(256) << 20; // plan memory of one cached plan at most
+
+static std::string plan_key(const pp_context *ctx, const Graph *g, const pp_device_desc *dev, int k_bound) {
+  const Knobs kn;
+  std::string k;
+  auto put = [&](const void *p, size_t n) { k.append(static_cast<const char *>(p), n); };
+  put(&g, sizeof(g));
+  const int32_t flags[6] = {k_bound, ctx->precision, ctx->no_minplus, ctx->no_fused, ctx->mp_conservative, dev->count};
+  put(flags, sizeof(flags));
+  put(&kn, sizeof(kn));
+  put(dev->compute_rates, static_cast<size_t>(dev->count) * 8);
+  put(dev->bandwidth, static_cast<size_t>(dev->count) * dev->count * 8);
+  return k;
+}
+
+// true: the call was served by a cached (or newly cached) prepared plan
+static bool run_plan_cached(pp_context *ctx, const std::shared_ptr<Graph> &g, const pp_device_desc *dev, int k_bound,
+                            int32_t *indices, pp_plan_result *res) {
+  const bool on = env_int("PARPLAN_PLAN_CACHE", 1) != 0;
+  if (!on || ctx->nranks > 1 || dev->count < 1 || !dev->compute_rates || !dev->bandwidth) return false;
+  if (!ctx->plan_cache) ctx->plan_cache = std::make_shared<PlanCache>();
+  PlanCache &pc = *static_cast<PlanCache *>(ctx->plan_cache.get());
+  const std::string key = plan_key(ctx, g.get(), dev, k_bound);
+  PP_CUDA(cudaSetDevice(ctx->device));
+  for (auto &e : pc.entries)
+    if (e.key == key) {
+      e.used = ++pc.tick;
+      launch(e.P.get(), true);
+      fetch(e.P.get(), indices, res);
+      return true;
+    }
+  const auto it = std::find(pc.seen.begin(), pc.seen.end(), key);
+  if (it == pc.seen.end()) {
+    pc.seen.push_back(key);
+    if (pc.seen.size() > 16) pc.seen.erase(pc.seen.begin());
+    return false;
+  }
+  pc.seen.erase(it);
+  auto P = std::make_unique<pp_prepared>();
+  P->ctx = ctx;
+  P->g = g.get();
+  P->transient = false;
+  prepare(P.get(), dev, k_bound);
+  const bool keep = P->dmem.n + P->dscratch.n <= kPlanCacheMaxBytes;
+  if (keep) capture(P.get());
+  launch(P.get(), true);
+  fetch(P.get(), indices, res);
+  if (!keep) return true;
+  if (pc.entries.size() >= kPlanCacheEntries) { // least recently used out
+    auto lru = std::min_element(pc.entries.begin(), pc.entries.end(),
+                                [](const PlanCache::Entry &a, const PlanCache::Entry &b) { return a.used < b.used; });
+    PP_CUDA(cudaStreamSynchronize(ctx->stream));
+    pc.entries.erase(lru);
+  }
+  pc.entries.push_back(PlanCache::Entry{key, g, std::move(P), ++pc.tick});
+  return true;
+}
+
 // PARPLAN_WAVE_TRACE: per-wave and per-block globaltimer stamps of the fused
 // kernel (st: its phase stamps), printed to stderr by pp_plan_profile
 static void print_wave_trace(pp_prepared *P, const std::vector<uint64_t> &st, int waves) {
@@ -285,7 +368,8 @@ pp_status pp_plan(pp_context *ctx, const pp_graph *g, const pp_device_desc *dev,
                   pp_plan_result *res) {
   return guard([&] {
     PP_REQUIRE(ctx && g && dev && indices, "pp_plan: null argument");
-    run_plan(ctx, const_cast<pp_graph *>(g)->impl, nullptr, dev, k_bound, indices, res);
+    if (!run_plan_cached(ctx, g->own, dev, k_bound, indices, res))
+      run_plan(ctx, const_cast<pp_graph *>(g)->impl, nullptr, dev, k_bound, indices, res);
   });
 }
 

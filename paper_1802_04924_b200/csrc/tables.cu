@@ -120,6 +120,7 @@ pp_status pp_context_release_pools(pp_context *ctx) {
     PP_REQUIRE(ctx, "null context");
     PP_CUDA(cudaSetDevice(ctx->device));
     PP_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->plan_cache.reset();
     ctx->plan_pool.release();
     ctx->plan_scratch.release();
     ctx->scratch.release();
@@ -131,6 +132,7 @@ pp_status pp_context_destroy(pp_context *ctx) {
   if (!ctx) return PP_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->plan_cache.reset();
   ctx->desc.release();
   ctx->scratch.release();
   ctx->plan_pool.release();

@@ -261,3 +261,34 @@ def test_fused_knobs_match_oracle(gpu, knobs, monkeypatch):
             assert list(r.indices) == list(want.indices) and r.cost == want.cost
         r = P.plan(g, P.DeviceGraph.uniform(D), ctx=gpu.ctx)
         assert list(r.indices) == list(want.indices) and r.cost == want.cost
+
+
+def test_repeated_plan_calls_through_the_plan_cache(gpu):
+    """pp_plan keeps a prepared plan for a repeated (graph, devices, k_bound,
+    policy) call: the third and later calls replay it.  Interleaved device
+    counts, fresh graph objects (content-addressed) and a policy change must
+    each give the oracle's plan."""
+    import paper_1802_04924_b200 as P
+
+    ctx = P.Context(0)
+    want = {D: O.Instance.builtin("inception_chain", 32, "port").build_tables(D).plan() for D in (8, 16)}
+    for k in range(5):
+        for D in (16, 8):
+            g = P.builtin_model("inception_chain", 32)  # a new pp_graph per call
+            r = P.plan(g, P.DeviceGraph.uniform(D), ctx=ctx)
+            assert list(r.indices) == list(want[D].indices) and r.cost == want[D].cost, (k, D)
+    ctx.set_kernel_policy("unfused")
+    g = P.builtin_model("inception_chain", 32)
+    for _ in range(3):
+        r = P.plan(g, P.DeviceGraph.uniform(16), ctx=ctx)
+        assert list(r.indices) == list(want[16].indices) and r.cost == want[16].cost
+    # a different bandwidth is a different key (the tables change)
+    fast = P.DeviceGraph.uniform(16, bandwidth=2.5e10)
+    want_fast = None
+    for _ in range(3):
+        r = P.plan(g, fast, ctx=ctx)
+        want_fast = want_fast or r
+        assert list(r.indices) == list(want_fast.indices) and r.cost == want_fast.cost
+    ctx.release_pools()
+    r = P.plan(g, P.DeviceGraph.uniform(16), ctx=ctx)
+    assert list(r.indices) == list(want[16].indices) and r.cost == want[16].cost
