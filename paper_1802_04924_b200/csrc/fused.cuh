@@ -32,7 +32,8 @@ template <class T> struct FusedWave {
   const ChainDesc *chains;
   int64_t stage;    // chain segment: bytes per staging buffer
   const FoldDesc<T> *cfolds;
-  const uint16_t *fold_of; // per fold tile: its fold in `folds` (null: binary search)
+  const uint16_t *fold_of;  // per fold tile: its fold in `folds` (null: binary search)
+  const uint16_t *chain_of; // chain segment, per item: its chain in `chains` (null: binary search)
 };
 
 __device__ __forceinline__ int64_t first_item(int64_t rot) {
@@ -223,7 +224,8 @@ template <class T, bool kBuild> __global__ void __launch_bounds__(kFusedThreads,
     uint64_t *tr = a.trace && b0 == 0 ? a.trace + 16 * w : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = global_ns();
     if (W.n_chains)
-      for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x) chain_item<T>(W.chains, W.n_chains, W.cfolds, it, fused_smem, static_cast<size_t>(W.stage));
+      for (int64_t it = blockIdx.x; it < W.items; it += gridDim.x) chain_item<T>(W.chains, W.n_chains, W.cfolds, it, fused_smem, static_cast<size_t>(W.stage), nullptr,
+                                  W.chain_of);
     else if (!narrow || static_cast<int>(blockIdx.x) < a.nc)
       for (int64_t it = b0; it < W.items; it += step)
         wave_item<T>(W.folds, W.nf, W.ftiles, W.merges, W.nm, it, sm, narrow ? nullptr : &st, it == 0 ? tr : nullptr,

@@ -421,9 +421,11 @@ __device__ __forceinline__ void chain_scan(const T *ws, const T *cr, const T *t2
 // reader.
 template <class T>
 __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains, const FoldDesc<T> *cf, int64_t it,
-                                           unsigned char *smem, size_t stage, uint64_t *tr = nullptr) {
+                                           unsigned char *smem, size_t stage, uint64_t *tr = nullptr,
+                                           const uint16_t *chain_of = nullptr) {
   const bool stamp = tr && threadIdx.x == 0;
-  int lo = 0, hi = n_chains - 1;
+  // the item's chain: one load from the per-item index when the image has it
+  int lo = chain_of ? chain_of[it] : 0, hi = chain_of ? lo : n_chains - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (chains[mid].item_begin <= it)

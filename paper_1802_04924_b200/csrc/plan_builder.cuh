@@ -821,6 +821,15 @@ template <class T> void PlanBuilder<T>::image_phases(Image &im, Work &wk) {
       e.stage = static_cast<int64_t>(S.stage);
       e.chains = reinterpret_cast<const ChainDesc *>(db + off_image + oc);
       e.cfolds = reinterpret_cast<const FoldDesc<T> *>(db + off_image + of);
+      if (S.chains.size() > 1) { // per-item chain index (replaces a binary search per item)
+        PP_REQUIRE(S.chains.size() <= 65535, "too many chains in one segment");
+        std::vector<uint16_t> chain_of(static_cast<size_t>(S.items));
+        for (size_t q = 0; q < S.chains.size(); ++q) {
+          const int64_t i1 = q + 1 < S.chains.size() ? S.chains[q + 1].item_begin : S.items;
+          for (int64_t x = S.chains[q].item_begin; x < i1; ++x) chain_of[static_cast<size_t>(x)] = static_cast<uint16_t>(q);
+        }
+        e.chain_of = reinterpret_cast<const uint16_t *>(db + off_image + pk.put(chain_of));
+      }
       fw.push_back(e);
       double cells = 0.0;
       for (int x = S.ws; x <= S.we; ++x) cells += im.waves[static_cast<size_t>(x) - 1].cells;
