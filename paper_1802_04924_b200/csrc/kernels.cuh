@@ -346,11 +346,17 @@ template <class T> __device__ __forceinline__ unsigned bulk_bytes(const T *p, in
 // Thread 0: stream fold f's t2 and w into staging buffer `buf` (t2 at the
 // front, w after it at `w_at` bytes), completing on `bar`.
 template <class T>
-__device__ __forceinline__ void chain_stage(const FoldDesc<T> &f, unsigned char *buf, size_t w_at, uint64_t *bar) {
+__device__ __forceinline__ void chain_stage(const FoldDesc<T> &f, unsigned char *buf, size_t w_at, uint64_t *bar,
+                                            bool first) {
   const int64_t n2 = static_cast<int64_t>(f.nw) * f.nv;
-  // earlier generic reads of buf, and the generic stores that produced t2 / w
-  // (table build, earlier waves), happen before the async-proxy copies
-  fence_proxy_async_all();
+  // earlier generic reads of buf happen before the async-proxy copies; the
+  // first copies of an item also order the generic global stores that
+  // produced t2 / w (table build, earlier phases: every chain fold's t2 is
+  // written before its segment starts, w are node tables)
+  if (first)
+    fence_proxy_async_all();
+  else
+    fence_proxy_async();
   mbar_expect_tx(bar, bulk_bytes(f.t2, n2) + bulk_bytes(f.w, f.nw));
   bulk_range(reinterpret_cast<T *>(buf), f.t2, n2, bar);
   bulk_range(reinterpret_cast<T *>(buf + w_at), f.w, f.nw, bar);
@@ -458,8 +464,8 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
   __syncthreads();
   auto w_at = [&](int k) { return align16(static_cast<size_t>(fd[k].nw) * fd[k].nv * sizeof(T) + 16); };
   if (threadIdx.x == 0) { // folds 0 and 1 stream in now; fold k + 2 once fold k's scan frees its buffer
-    chain_stage<T>(fd[0], buf[0], w_at(0), &bar[0]);
-    if (c.n > 1) chain_stage<T>(fd[1], buf[1], w_at(1), &bar[1]);
+    chain_stage<T>(fd[0], buf[0], w_at(0), &bar[0], true);
+    if (c.n > 1) chain_stage<T>(fd[1], buf[1], w_at(1), &bar[1], false);
   }
   {
     const FoldDesc<T> &f0 = fd[0];
@@ -497,7 +503,7 @@ __device__ __forceinline__ void chain_item(const ChainDesc *chains, int n_chains
     if (stamp && k < 4) tr[4 * k + 3] = trace_ns();
     if (k + 2 < c.n && threadIdx.x == kFoldThreads - 1) { // buf[k & 1] is free again
       if (tr && k < 4) tr[16 + 2 * k] = trace_ns();
-      chain_stage<T>(fd[k + 2], buf[k & 1], w_at(k + 2), &bar[k & 1]);
+      chain_stage<T>(fd[k + 2], buf[k & 1], w_at(k + 2), &bar[k & 1], false);
       if (tr && k < 4) tr[17 + 2 * k] = trace_ns();
     }
     const bool last = k + 1 == c.n;
