@@ -89,7 +89,7 @@ template <class T> struct PanelSmem {
 // Row r of f_{k+1}.out depends on row r of f_k.out alone (Eq. 2 folds t1 row
 // by row), so one block carries a few rows through the whole chain in shared
 // memory: one grid barrier per segment instead of one per wave.
-constexpr int kChainRows = 4;  // rows per item (max)
+constexpr int kChainRows = 8;  // rows per item (max)
 constexpr int kChainMax = 128; // max nw / nv of a chain fold
 struct ChainDesc {
   int32_t first, n;  // folds [first, first + n) of the segment's fold list

@@ -683,20 +683,34 @@ template <class T> void PlanBuilder<T>::image_segments(Image &im, Work &wk) {
         chain_of_table[static_cast<size_t>(o.ne)] = c;
       }
     }
-    int64_t rows_total = 0;
-    int max_len = 0;
+    int max_len = 0, max_nw = 1;
     size_t stage = 0;
     for (const auto &m : members) {
-      rows_total += wk.folds[m.front()].nu;
       max_len = std::max(max_len, static_cast<int>(m.size()));
-      for (size_t q : m) stage = std::max(stage, chain_stage_bytes<T>(wk.folds[q].nw, wk.folds[q].nv));
+      for (size_t q : m) {
+        stage = std::max(stage, chain_stage_bytes<T>(wk.folds[q].nw, wk.folds[q].nv));
+        max_nw = std::max(max_nw, wk.folds[q].nw);
+      }
     }
-    const int64_t cap = 2 * int64_t(ctx->sms);
-    int rows = static_cast<int>(std::clamp<int64_t>((rows_total + cap - 1) / cap, 1, kChainRows));
-    // unwind path tables for chains of >= 3 folds, when the argmins fit in shared memory
-    bool path = max_len >= 3 && kn.chain_path;
-    while (rows > 1 && chain_smem_bytes<T>(rows, max_len, stage, path) > limit) --rows;
-    if (path && chain_smem_bytes<T>(rows, max_len, stage, path) > limit) path = false;
+    // rows per item: the fewest rounds of items over the resident blocks (2
+    // per SM; 1 with the large shared-memory layout) times the per-fold scan
+    // length, kChainGroups / rows warps sharing a row's j range, plus a fixed
+    // per-fold cost of ~14 j steps (measured: I16's first segment runs 6-row
+    // items in one round faster than 4-row items in two)
+    const int64_t blocks = (limit > chain_smem_max ? 1 : 2) * int64_t(ctx->sms);
+    const bool want_path = max_len >= 3 && kn.chain_path; // unwind path tables for chains of >= 3 folds
+    int rows = 1;
+    bool path = false;
+    int64_t best = INT64_MAX;
+    for (int R = 1; R <= std::clamp(kn.chain_rows, 1, kChainRows); ++R) {
+      const bool pr = want_path && chain_smem_bytes<T>(R, max_len, stage, true) <= limit;
+      if (chain_smem_bytes<T>(R, max_len, stage, pr) > limit) break;
+      int64_t items = 0;
+      for (const auto &m : members) items += (wk.folds[m.front()].nu + R - 1) / R;
+      const int wpr = std::max(1, kChainGroups / R);
+      const int64_t cost = (items + blocks - 1) / blocks * (14 + (max_nw + wpr - 1) / wpr);
+      if (cost < best || (cost == best && pr && !path)) best = cost, rows = R, path = pr;
+    }
     sg.smem = chain_smem_bytes<T>(rows, max_len, stage, path);
     sg.stage = stage;
     for (const auto &m : members) {

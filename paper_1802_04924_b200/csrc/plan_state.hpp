@@ -45,6 +45,7 @@ struct Knobs {
   int chains = env_int("PARPLAN_CHAINS", 1);
   int chain_path = env_int("PARPLAN_CHAIN_PATH", 1); // unwind path tables for chains of >= 3 folds
   int chain_min_waves = std::max(2, env_int("PARPLAN_CHAIN_MIN_WAVES", 2));
+  int chain_rows = env_int("PARPLAN_CHAIN_ROWS", 8); // rows per chain item at most (the cost model picks)
   int chain_smem_kb = env_int("PARPLAN_CHAIN_SMEM_KB", 110);
   int chain_smem_big_kb = env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216);
   int chain_big_gain = env_int("PARPLAN_CHAIN_BIG_GAIN", 6); // barriers a one-CTA-per-SM segment layout must save

@@ -26,6 +26,7 @@ for model, D in [("inception_chain", 16), ("inception_chain", 64), ("vgg16", 16)
         prep.launch()
         s1.record(stream)
         prep.fetch()
+        s1.synchronize()
         if k >= 5:
             ms.append(s0.elapsed_time(s1))
     e2e = []
