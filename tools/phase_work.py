@@ -1,5 +1,6 @@
-import sys
-sys.path.insert(0, "/root/repo")
+"""Per-phase device time and work (cells) of prepared I64 and I16 plans (profile())."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1802_04924_b200 as P
 ctx = P.Context(0)
 for D in (64, 16):
