@@ -39,7 +39,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL's version line too: stdout is the one JSON line
 
 METRIC = "Inception-v3 optimal-config search ms; min-plus cell-updates/s vs FP32 roofline"
 PAPER_MS = 100.0  # PAPER.md:80 "about 100 ms" for Inception-v3 (120 nodes) on 16 GPUs
@@ -520,7 +521,7 @@ def sharded(P, args, local, stream, flush):
         "device_ms": PD.max_over_ranks(statistics.mean(ms), device="cuda"),
         "matches_reference": bool(gold and [int(x) for x in r.indices] == gold["indices"]
                                   and float(r.cost).hex() == gold["cost"]),
-        "note": "K1/K2 on every rank, row-sharded DP; latency-bound, sharding is not expected to help (SURVEY §8e)"}
+        "note": "K1 edge-sharded + broadcast, K2 on every rank, row-sharded DP, distributed unwind; latency-bound, sharding is not expected to help (SURVEY §8e)"}
     del prep
     # the min-plus config-5 graph at C = shard_c
     C = args.shard_c
