@@ -40,7 +40,16 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL's version line too: stdout is the one JSON line
+
+# stdout carries exactly one JSON line: libraries that print to fd 1 (NCCL's
+# version banner, ...) go to stderr; the line is written to the saved stdout
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
 
 METRIC = "Inception-v3 optimal-config search ms; min-plus cell-updates/s vs FP32 roofline"
 PAPER_MS = 100.0  # PAPER.md:80 "about 100 ms" for Inception-v3 (120 nodes) on 16 GPUs
@@ -189,7 +198,7 @@ def run_reference(args):
         "result": {"cost": res.cost, "node_eliminations": res.node_eliminations,
                    "edge_eliminations": res.edge_eliminations},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -735,7 +744,7 @@ def run_ours(args):
         line["result"]["matches_cpu_reference"] = bool(
             list(res_ref.indices) == list(r.indices) and res_ref.cost == r.cost)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
