@@ -216,7 +216,8 @@ struct PlanCache {
     uint64_t used = 0;
   };
   std::vector<Entry> entries;
-  std::vector<std::string> seen; // keys planned once: a second call caches
+  std::vector<std::string> seen;    // keys planned once: a second call caches
+  std::vector<std::string> too_big; // keys whose plans exceed kPlanCacheMaxBytes: the pooled one-shot path
   uint64_t tick = 0;
 };
 constexpr size_t kPlanCacheEntries = 4;
@@ -251,6 +252,7 @@ static bool run_plan_cached(pp_context *ctx, const std::shared_ptr<Graph> &g, co
       fetch(e.P.get(), indices, res);
       return true;
     }
+  if (std::find(pc.too_big.begin(), pc.too_big.end(), key) != pc.too_big.end()) return false;
   const auto it = std::find(pc.seen.begin(), pc.seen.end(), key);
   if (it == pc.seen.end()) {
     pc.seen.push_back(key);
@@ -267,7 +269,11 @@ static bool run_plan_cached(pp_context *ctx, const std::shared_ptr<Graph> &g, co
   if (keep) capture(P.get());
   launch(P.get(), true);
   fetch(P.get(), indices, res);
-  if (!keep) return true;
+  if (!keep) {
+    pc.too_big.push_back(key);
+    if (pc.too_big.size() > 16) pc.too_big.erase(pc.too_big.begin());
+    return true;
+  }
   if (pc.entries.size() >= kPlanCacheEntries) { // least recently used out
     auto lru = std::min_element(pc.entries.begin(), pc.entries.end(),
                                 [](const PlanCache::Entry &a, const PlanCache::Entry &b) { return a.used < b.used; });
