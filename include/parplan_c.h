@@ -274,10 +274,15 @@ pp_status pp_plan_launch(pp_prepared *p, int32_t upload_inputs);
 pp_status pp_plan_fetch(pp_prepared *p, int32_t *indices, pp_plan_result *res);
 pp_status pp_plan_destroy(pp_prepared *p);
 /* Runs the prepared device work once with a CUDA event between launches and
- * reports, per step: device ms, kind (0 K1/K2 tables, 1 wave of K3/K4 folds
- * and merges, 2 K5 enumeration, 3 unwind + cost re-sum, 4 result D2H) and
- * algorithmic work (table cells for 0; sum of nu*nw*nv fold cells plus merge
- * cells for 1; candidates for 2; bytes for 4).  n_steps receives the count. */
+ * reports, per step: device ms, kind and algorithmic work (table cells for
+ * K1/K2; sum of nu*nw*nv fold cells plus merge cells for folds; candidates for
+ * K5; bytes for collectives).  n_steps receives the count.  Kinds: 0 K1/K2
+ * tables, 1 wave of K3/K4 folds and merges, 2 K5 enumeration, 3 unwind + cost
+ * re-sum, 5 min-plus memsets, 6 mp_prep / mp64_prep, 7 mp_minima, 8 mp_fold,
+ * 9 mp_merge, 10 fused kernel (expanded into its phases: 11 tables, 12 wave,
+ * 13 enumerate, 14 finish, 16 chain segment, then 10 for the residual),
+ * 15 all-gather, 17 mp_chain, 18 mp64_fold, 19 K1 edge-range broadcast,
+ * 20 all-reduce of the optimistic-cap overflow flag (row-sharded plans). */
 pp_status pp_plan_profile(pp_prepared *p, int32_t cap, double *step_ms, int32_t *step_kind, double *step_work,
                           int32_t *n_steps);
 

@@ -652,7 +652,7 @@ class PreparedPlan:
         names = {0: "tables", 1: "wave", 2: "enumerate", 3: "finish", 4: "d2h", 5: "memset", 6: "mp_prep",
                  7: "mp_minima", 8: "mp_fold", 9: "mp_merge", 10: "fused", 11: "fused.tables",
                  12: "fused.wave", 13: "fused.enumerate", 14: "fused.finish", 15: "allgather", 16: "fused.chain",
-                 17: "mp_chain", 18: "mp64_fold", 19: "tables.broadcast"}
+                 17: "mp_chain", 18: "mp64_fold", 19: "tables.broadcast", 20: "allreduce.ovf"}
         return [(names[int(k)], float(m), float(w)) for k, m, w in zip(kind, ms, work)]
 
     def __del__(self):

@@ -32,6 +32,7 @@ const Nccl &nccl() {
     n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
     n.AllGather = reinterpret_cast<decltype(n.AllGather)>(sym("ncclAllGather"));
     n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(sym("ncclBroadcast"));
+    n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(sym("ncclAllReduce"));
     n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
     n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(sym("ncclGroupEnd"));
     n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
@@ -94,6 +95,10 @@ void all_gather(pp_context *ctx, const void *send, void *recv, size_t bytes, cud
 
 void broadcast(pp_context *ctx, void *buf, size_t bytes, int root, cudaStream_t st) {
   PP_NCCL(nccl().Broadcast(buf, buf, bytes, ncclUint8, root, static_cast<ncclComm_t>(ctx->comm), st));
+}
+
+void all_reduce_max(pp_context *ctx, int32_t *buf, size_t count, cudaStream_t st) {
+  PP_NCCL(nccl().AllReduce(buf, buf, count, ncclInt32, ncclMax, static_cast<ncclComm_t>(ctx->comm), st));
 }
 
 void group_start() { PP_NCCL(nccl().GroupStart()); }

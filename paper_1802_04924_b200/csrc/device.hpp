@@ -138,6 +138,7 @@ namespace pp {
 void comm_destroy(pp_context *ctx);
 void all_gather(pp_context *ctx, const void *send, void *recv, size_t bytes, cudaStream_t st);
 void broadcast(pp_context *ctx, void *buf, size_t bytes, int root, cudaStream_t st); // in place
+void all_reduce_max(pp_context *ctx, int32_t *buf, size_t count, cudaStream_t st);   // in place
 void group_start();
 void group_end();
 

@@ -26,7 +26,7 @@ struct MinplusPlan {
     const std::vector<int32_t> &rows, &cols; // configs of each table's source / destination node
     std::function<int(int)> nu_eff;          // rows of a table this rank works on
     bool shard;                              // row-sharded plan
-    bool conservative;                       // proven caps only (after an optimistic overflow, on request, sharded)
+    bool conservative;                       // proven caps only (after an optimistic overflow, on request)
     bool no_minplus;                         // kernel policy: generic folds only
     int sms;
     bool chains;                             // mp_chain runs (PARPLAN_MP_CHAIN)
@@ -57,6 +57,7 @@ struct MinplusPlan {
   // sections: per-wave operand blocks; persistent = stream-K part slots | tile
   // counters (0 at rest) | ra, cb (0xFF.. before use) | chain B''
   size_t bytes = 0, part = 0, cnt = 0, ra = 0, cb = 0, chainb = 0;
+  bool any_opt = false; // some large fold runs with an optimistic cap (the overflow flag matters)
   size_t pbytes() const { return part + cnt + ra + cb + chainb; }
 
   template <class T> void build(const In &in);
@@ -107,6 +108,7 @@ template <class T> void MinplusPlan::build(const In &in) {
       // optimistic JB 6 (cap 511, checked in the epilogue) unless conservative
       if (!conservative) fold_opt[oi] = 1, fold_jb[oi] = nw >= kMpWideNw ? kMpOptJBWide : kMpOptJB;
       large[oi] = nu >= 64 && nv >= 64 && nw >= 64 && fold_jb[oi] > 0 && !in.no_minplus;
+      any_opt = any_opt || (large[oi] && fold_opt[oi]);
       if (large[oi] && nu_eff(op.e1) > 0) {
         mp_consumer[a] = static_cast<int>(oi);
         mp_consumer2[b2] = static_cast<int>(oi);

@@ -116,10 +116,23 @@ static void launch(pp_prepared *P, bool upload);
 // fixed-point tables reach the min-plus kernels, and those are given
 // (plan_with_tables), so no table build is repeated.
 static void rerun_conservative(pp_prepared *P) {
-  PP_CUDA(cudaEventSynchronize(P->ctx->ev1));
+  pp_context *ctx = P->ctx;
+  PP_CUDA(cudaEventSynchronize(ctx->ev1));
   if (std::getenv("PARPLAN_TRACE")) std::fprintf(stderr, "[parplan] optimistic operand cap reached: re-planning with proven caps\n");
+  const bool ranks = P->nranks > 1 && ctx->comm;
+  if (ranks) {
+    // every rank reruns (the flag was all-reduced); the plan memory is
+    // reallocated, so first wait until no rank's finish still reads it
+    DBuf<int32_t> word(1);
+    PP_CUDA(cudaMemsetAsync(word.p, 0, 4, ctx->stream));
+    all_reduce_max(ctx, word.p, 1, ctx->stream);
+    PP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (void *p : P->ipc_opened) cudaIpcCloseMemHandle(p);
+    P->ipc_opened.clear();
+  }
   P->mp_conservative = true;
   PlanBuilder<int32_t>(P, nullptr).build(P->k_bound);
+  if (ranks) exchange_peers(P);
   P->uploaded = false;
   if (!P->transient) capture(P);
   launch(P, true);
@@ -504,12 +517,30 @@ static void run_group(std::vector<pp_prepared *> &Ps) {
     for (int r = 0; r < n; ++r) {
       pp_prepared &P = *Ps[static_cast<size_t>(r)];
       size_t &i = pos[static_cast<size_t>(r)];
-      while (i < P.steps.size() && P.step_kind[i] != 15 && P.step_kind[i] != 19) P.steps[i++](P.ctx->stream);
+      while (i < P.steps.size() && P.step_kind[i] != 15 && P.step_kind[i] != 19 && P.step_kind[i] != 20)
+        P.steps[i++](P.ctx->stream);
       PP_CUDA(cudaEventRecord(ev[static_cast<size_t>(r)], P.ctx->stream));
       at_gather += i < P.steps.size();
     }
     if (at_gather == 0) break;
     PP_REQUIRE(at_gather == n, "virtual ranks disagree on the all-gather schedule");
+    if (Ps[0]->step_kind[pos[0]] == 20) { // overflow flags: OR over the ranks, on the host (a test transport)
+      int32_t any = 0;
+      for (int r = 0; r < n; ++r) {
+        pp_prepared &P = *Ps[static_cast<size_t>(r)];
+        PP_REQUIRE(P.step_kind[pos[static_cast<size_t>(r)]] == 20, "virtual ranks disagree on the collective schedule");
+        int32_t v = 0;
+        PP_CUDA(cudaStreamSynchronize(P.ctx->stream));
+        PP_CUDA(cudaMemcpy(&v, std::get<0>(P.gather_lists[k][0]), 4, cudaMemcpyDeviceToHost));
+        any = std::max(any, v);
+      }
+      for (int r = 0; r < n; ++r) {
+        pp_prepared &P = *Ps[static_cast<size_t>(r)];
+        PP_CUDA(cudaMemcpy(std::get<1>(P.gather_lists[k][0]), &any, 4, cudaMemcpyHostToDevice));
+        ++pos[static_cast<size_t>(r)];
+      }
+      continue;
+    }
     for (int r = 0; r < n; ++r) {
       pp_prepared &P = *Ps[static_cast<size_t>(r)];
       for (int q = 0; q < n; ++q)
@@ -595,6 +626,19 @@ pp_status pp_vgroup_plan(pp_vgroup *grp, const pp_graph *g, const pp_device_desc
       own.push_back(std::move(P));
     }
     run_group(Ps);
+    { // an optimistic operand cap was reached on some rank (the flag is OR-ed over the ranks): all rerun
+      for (pp_prepared *P : Ps) PP_CUDA(cudaStreamSynchronize(P->ctx->stream));
+      uint32_t ovf = 0;
+      std::memcpy(&ovf, Ps[0]->hbase + Ps[0]->off_ovf, 4);
+      if (ovf && !Ps[0]->mp_conservative && Ps[0]->t->mode != kFP64) {
+        for (pp_prepared *P : Ps) {
+          P->mp_conservative = true;
+          PlanBuilder<int32_t>(P, nullptr).build(P->k_bound);
+          P->uploaded = false;
+        }
+        run_group(Ps);
+      }
+    }
     fetch(Ps[0], indices, res);
     for (size_t r = 1; r < Ps.size(); ++r) { // every rank unwinds the same plan
       std::vector<int32_t> mine(static_cast<size_t>(g->impl.nl));

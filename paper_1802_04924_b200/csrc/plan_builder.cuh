@@ -317,7 +317,7 @@ template <class T> void PlanBuilder<T>::early_table_build() {
 // ---- stage 3: large folds (U16 fixed point / FP64) -------------------------------
 template <class T> void PlanBuilder<T>::plan_minplus() {
   mp.build<T>(MinplusPlan::In{s, t, mem.rows, mem.cols, [this](int id) { return mem.nu_eff(id); }, mem.shard,
-                              P->mp_conservative || ctx->mp_conservative || mem.shard, ctx->no_minplus, ctx->sms,
+                              P->mp_conservative || ctx->mp_conservative, ctx->no_minplus, ctx->sms,
                               kn.mp_chain != 0, kn.mp_chain_min, mem.prod_wave});
   // dynamic shared memory allowances: per device, so set on every prepare (cheap)
   for (const MpRun &run : mp.runs)

@@ -396,6 +396,15 @@ template <class T> void PlanBuilder<T>::emit_steps(const Image &im) {
   emit_minima(im);
   emit_waves(im);
   emit_gathers(im.final_gathers);
+  if (mem.shard && mp.any_opt) { // every rank sees any rank's optimistic-cap overflow (fetch reruns them all)
+    pp_context *c = ctx;
+    int32_t *ovf = reinterpret_cast<int32_t *>(db + off_image + im.oOvf);
+    step(20, 4.0, [c, ovf](cudaStream_t st) {
+      PP_REQUIRE(c->comm, "row-sharded plan without a communicator (virtual ranks run through pp_vgroup)");
+      all_reduce_max(c, ovf, 1, st);
+    }, 0);
+    P->gather_lists.push_back(CopyList{{ovf, ovf, 4}}); // kind 20: the flag word (virtual ranks OR it on the host)
+  }
   const FinishArgs fa = finish_args(im);
   P->nblk_dbg = nblk;
   P->ngroups_dbg = im.nG;

@@ -44,6 +44,25 @@ def main():
             fails.append(f"no all-gather in sharded plan C={C}")
         prep.launch()
         check(f"prepared sharded C={C}", prep.fetch(), b)
+    # optimistic operand caps overflow on some rank: all ranks re-plan with proven caps
+    import numpy as np
+
+    m = 96
+    layers = [P.Layer("u", "input", [4, 1, 1])] + [P.Layer(f"n{i}", "softmax") for i in range(1, 3)]
+    g = P.ComputationGraph.create(layers, [[]] + [[layers[i - 1].id] for i in range(1, 3)], 8)
+    x1 = np.full((m, m), 2000 / 64.0)
+    x1[np.arange(m), np.arange(m)] = 0.0
+    x2 = np.full((m, m), 2000 / 64.0)
+    x2[(np.arange(m) + 1) % m, np.arange(m)] = 0.0
+    rng = np.random.default_rng(7)
+    node = [rng.integers(0, 64, m) / 64.0, np.zeros(m), rng.integers(0, 64, m) / 64.0]
+    cat = [np.tile([1, 1, 1, 1], (m, 1)) for _ in range(3)]
+    want = P.plan_with_tables(g, P.upload_cost_tables(g, cat, node, [x1, x2], solo))
+    ts = P.upload_cost_tables(g, cat, node, [x1, x2], shard_ctx)
+    check("overflow one-shot", P.plan_with_tables(g, ts), want)
+    prep = P.PreparedPlan(g, tables=ts, ctx=shard_ctx)
+    prep.launch()
+    check("overflow prepared", prep.fetch(), want)
     for seed in range(20):
         g, t = P.random_series_parallel_graph(seed, 10 + 9 * seed, 3, 0.4, 4, ctx=shard_ctx)
         cat, node, _, _, xfer = t.download()

@@ -109,8 +109,9 @@ def test_virtual_ranks_builtin_match_reference(gpu, n, case):
 @pytest.mark.parametrize("n", [2, 4, 8])
 @pytest.mark.parametrize("C", [256, 700])
 def test_virtual_ranks_config5_match_single_gpu(gpu, n, C):
-    """Config-5 graph (U16 min-plus folds, row-sharded with proven caps): the
-    same indices and cost as one GPU; at C = 256 also the real reference."""
+    """Config-5 graph (U16 min-plus folds, row-sharded, optimistic operand caps
+    with the overflow flag OR-ed over the ranks): the same indices and cost as
+    one GPU; at C = 256 also the real reference."""
     import json
 
     import paper_1802_04924_b200 as P
@@ -122,6 +123,34 @@ def test_virtual_ranks_config5_match_single_gpu(gpu, n, C):
     if C == 256:
         gold = next(c for c in _gold()["synthetic"] if c["configs"] == 256)
         assert [int(x) for x in r.indices] == gold["indices"] and float(r.cost).hex() == gold["cost"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3])
+def test_virtual_ranks_optimistic_cap_overflow_reruns(gpu, n):
+    """Every fold minimum is 2000 units, above the optimistic operand cap: some
+    rank's device check fires, the flag is OR-ed over the ranks (kind-20 step)
+    and every rank re-plans with proven caps -- the generic fold's result."""
+    import numpy as np
+
+    import paper_1802_04924_b200 as P
+
+    m = 96
+    layers = [P.Layer("u", "input", [4, 1, 1])] + [P.Layer(f"n{i}", "softmax") for i in range(1, 3)]
+    g = P.ComputationGraph.create(layers, [[]] + [[layers[i - 1].id] for i in range(1, 3)], 8)
+    t1 = np.full((m, m), 2000 / 64.0)
+    t1[np.arange(m), np.arange(m)] = 0.0
+    t2 = np.full((m, m), 2000 / 64.0)
+    t2[(np.arange(m) + 1) % m, np.arange(m)] = 0.0
+    rng = np.random.default_rng(7)
+    node = [rng.integers(0, 64, m) / 64.0, np.zeros(m), rng.integers(0, 64, m) / 64.0]
+    cat = [np.tile([1, 1, 1, 1], (m, 1)) for _ in range(3)]
+    slow = P.Context(0)
+    slow.set_kernel_policy("generic")
+    want = P.plan_with_tables(g, P.upload_cost_tables(g, cat, node, [t1, t2], slow))
+    tf = P.upload_cost_tables(g, cat, node, [t1, t2], gpu.ctx)
+    r = P.VirtualRanks(n).plan(g, tables=tf)
+    assert list(r.indices) == list(want.indices) and r.cost == want.cost
 
 
 @pytest.mark.gpu
