@@ -23,8 +23,9 @@ inline int env_int(const char *name, int dflt) {
 }
 
 // Tuning knobs, read once per prepare (A/B experiments in one process).  The
-// defaults are the measured best; the non-default settings stay selectable
-// because the parity tests run every plan shape through them.
+// defaults are the measured best; the settings read from the environment stay
+// selectable because the parity tests run every plan shape through them.  The
+// plain constants are fixed tuning values (they used to be switches).
 struct Knobs {
   // fused kernel
   int cluster = env_int("PARPLAN_CLUSTER", 1);            // thread-block cluster size of the cooperative launch
@@ -34,24 +35,24 @@ struct Knobs {
   int split_build = env_int("PARPLAN_SPLIT_BUILD", 1);    // prepared plans: table build as its own launch
   int early_build = env_int("PARPLAN_EARLY_BUILD", 1);    // one-shot plans: table build launched before the image
   int stage = env_int("PARPLAN_STAGE", 1);                // stage the next wave's operands before the barrier
-  int rotate = env_int("PARPLAN_ROTATE", 1);              // rotate item -> block assignment across waves
+  int rotate = 1;                                         // rotate item -> block assignment across waves
   int blocks_per_sm = env_int("PARPLAN_FUSED_BLOCKS_PER_SM", 0); // 0: occupancy limit
   int wave_trace = env_int("PARPLAN_WAVE_TRACE", 0);      // per-wave globaltimer stamps (pp_plan_profile prints)
   // generic folds
   int panel = env_int("PARPLAN_PANEL", 1);           // small waves: 4/8-row panel tiles
-  int panel_side = env_int("PARPLAN_PANEL_SIDE", 0); // force a panel side (0: smallest that fills the GPU)
+  int panel_side = 0;                                // forced panel side (0: the smallest that fills the GPU)
   int merge_fuse = env_int("PARPLAN_MERGE_FUSE", 1); // merge absorption into fold epilogues
   // chain segments (fused kernel)
   int chains = env_int("PARPLAN_CHAINS", 1);
-  int chain_path = env_int("PARPLAN_CHAIN_PATH", 1); // unwind path tables for chains of >= 3 folds
-  int chain_min_waves = std::max(2, env_int("PARPLAN_CHAIN_MIN_WAVES", 2));
+  int chain_path = 1;                                // unwind path tables for chains of >= 3 folds
+  int chain_min_waves = 2;                           // shortest segment (waves)
   int chain_rows = env_int("PARPLAN_CHAIN_ROWS", 8); // rows per chain item at most (the cost model picks)
-  int chain_smem_kb = env_int("PARPLAN_CHAIN_SMEM_KB", 110);
-  int chain_smem_big_kb = env_int("PARPLAN_CHAIN_SMEM_BIG_KB", 216);
-  int chain_big_gain = env_int("PARPLAN_CHAIN_BIG_GAIN", 6); // barriers a one-CTA-per-SM segment layout must save
+  int chain_smem_kb = 110;                           // segment shared memory at two CTAs per SM
+  int chain_smem_big_kb = 216;                       // ... at one CTA per SM
+  int chain_big_gain = 6;                            // barriers a one-CTA-per-SM segment layout must save
   // large min-plus folds
   int mp_chain = env_int("PARPLAN_MP_CHAIN", 1);                           // mp_chain runs
-  int mp_chain_min = std::max(1, env_int("PARPLAN_MP_CHAIN_MIN", 4));      // shortest run worth a chain launch
+  int mp_chain_min = 4;                                                    // shortest run worth a chain launch
 };
 
 // PARPLAN_TRACE=2: host-side timing of the build stages

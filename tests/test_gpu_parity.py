@@ -292,3 +292,19 @@ def test_repeated_plan_calls_through_the_plan_cache(gpu):
     ctx.release_pools()
     r = P.plan(g, P.DeviceGraph.uniform(16), ctx=ctx)
     assert list(r.indices) == list(want[16].indices) and r.cost == want[16].cost
+
+
+def test_plan_cache_eviction_keeps_results(gpu):
+    """Six keys through a four-entry plan cache, twice round: evicted plans are
+    rebuilt and every call still returns its key's first (uncached) result."""
+    import paper_1802_04924_b200 as P
+
+    ctx = P.Context(0)
+    g = P.builtin_model("inception_chain(3)", 32)
+    devs = [P.DeviceGraph.uniform(8, bandwidth=1.25e10 * (1 + k)) for k in range(6)]
+    first = [P.plan(g, d, ctx=ctx) for d in devs]
+    for _ in range(2):
+        for d, f in zip(devs, first):
+            for _ in range(3):
+                r = P.plan(g, d, ctx=ctx)
+                assert list(r.indices) == list(f.indices) and r.cost == f.cost

@@ -14,4 +14,4 @@ for _ in range(3):
     prep.launch(); r = prep.fetch(); ms.append(r.device_ms)
 agg = collections.Counter()
 for k, m, w in prep.profile(): agg[k] += m
-print(os.environ.get("PARPLAN_MP_SPLIT_PENALTY", "default"), "plan ms", round(min(ms), 2), {k: round(v, 2) for k, v in agg.items()}, "cost", r.cost)
+print("plan ms", round(min(ms), 2), {k: round(v, 2) for k, v in agg.items()}, "cost", r.cost)
