@@ -126,6 +126,22 @@ def test_virtual_ranks_config5_match_single_gpu(gpu, n, C):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n,C", [(2, 600), (4, 600), (2, 1100)])
+def test_virtual_ranks_fp64_large_folds_match_single_gpu(gpu, n, C):
+    """Uncertified FP64 tables, row-sharded (at C=1100 on 2 ranks each rank's
+    550 rows still take the mp64 fold): same IEEE result and argmins as one GPU."""
+    import paper_1802_04924_b200 as P
+
+    g = P.series_parallel_graph(3, 40, 0.4)
+    ctx = P.Context(0)
+    t = P.synthetic_cost_tables64(g, C, seed=9, ctx=ctx)
+    one = P.plan_with_tables(g, t)
+    assert one.precision == "fp64"
+    r = P.VirtualRanks(n).plan(g, tables=t)
+    assert list(r.indices) == list(one.indices) and r.cost == one.cost
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n", [2, 3])
 def test_virtual_ranks_optimistic_cap_overflow_reruns(gpu, n):
     """Every fold minimum is 2000 units, above the optimistic operand cap: some
