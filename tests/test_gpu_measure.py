@@ -32,8 +32,16 @@ def test_measured_costs_feed_the_planner(gpu, tmp_path):
     assert all(np.asarray(node[g.layer_id(l)]).max() > 0 for l in range(g.n_layers) if kinds[l] in (1, 2, 3))
 
     # planning on the measured tables, two ways
-    direct = P.plan_with_tables(g, P.upload_cost_tables(g, catalog, [np.asarray(node[g.layer_id(l)]) for l in
-                                                                     range(g.n_layers)], xfer, ctx=gpu.ctx))
+    measured = [np.asarray(node[g.layer_id(l)]) for l in range(g.n_layers)]
+    direct = P.plan_with_tables(g, P.upload_cost_tables(g, catalog, measured, xfer, ctx=gpu.ctx))
+    # ... and the oracle on the same (uncertified FP64) tables: bit-exact
+    import oracle as O
+
+    for kind in ("port", "reference"):
+        if not O.available(kind):
+            continue
+        want = O.Instance.builtin("lenet5", 32, kind).set_tables(catalog, measured, xfer).plan()
+        assert list(direct.indices) == list(want.indices) and direct.cost == want.cost, kind
     path = tmp_path / "measured.json"
     path.write_text(json.dumps(doc))
     if not os.path.exists(CLI):
